@@ -1,0 +1,108 @@
+/*
+ * permkit_b200.h -- C ABI of the B200-native Gray-walk permanent kernels.
+ *
+ * The entry points replace the inner machinery of the reference package
+ * permkit (/root/reference/pkg/src/permkit), whose Python surface
+ * (permanent, perm_nw, perm_spa, permanent_chunked, run_range, execute_plan)
+ * is mirrored one to one by the Python package paper_2502_16577_b200 on top
+ * of this ABI (see INTEGRATION.md for the ctypes binding a permkit
+ * maintainer would add).
+ *
+ * Conventions
+ *   - All arrays are host memory, C contiguous, owned by the caller. The
+ *     library copies what it needs to the device on every call (matrices are
+ *     at most 62*63*16 bytes) and keeps only per-device workspace.
+ *   - Calls are synchronous and thread safe; results go to caller buffers.
+ *   - Every function returns PK_OK (0) or a PK_ERR_* code; pk_last_error()
+ *     then holds a message (thread local). There is no CPU fallback: a
+ *     missing or failing device is PK_ERR_CUDA.
+ *   - Iterates follow the reference: g in [1, 2^(n-1) - 1]; g = 0 (the
+ *     initial product) is never part of a range (parallel.py:232-289).
+ *   - A range partial is what run_range returns (parallel.py:144-159):
+ *     a double-double (hi, lo) for real kinds, (re, im) for complex, and the
+ *     exact signed y-space integer (two's complement, little-endian 64-bit
+ *     words) for the integer kind.
+ */
+#ifndef PERMKIT_B200_H
+#define PERMKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_ABI_VERSION 1
+
+/* status codes -> permkit exceptions (errors.py:11-47) */
+#define PK_OK 0
+#define PK_ERR_ARG 1        /* ValueError: bad n, range, pointer or count    */
+#define PK_ERR_POLICY 2     /* PolicyError (kernels.py:309-310)               */
+#define PK_ERR_STRUCTURE 3  /* StructureError: inconsistent CCS arrays        */
+#define PK_ERR_IMPOSSIBLE 4 /* ImpossibleError: n > 63 (matrix.py:35-42)      */
+#define PK_ERR_CUDA 5       /* device missing or a CUDA call failed           */
+#define PK_ERR_OVERFLOW 6   /* exact integer path cannot represent the values */
+
+/* accumulator policies, same codes as _loops.py:27-30 */
+#define PK_POLICY_DD 0
+#define PK_POLICY_KAHAN 1
+#define PK_POLICY_DQ 2
+#define PK_POLICY_QQ 3
+
+/* flags */
+#define PK_FLAG_EXACT 1u /* per-chunk arithmetic identical to the reference loop
+                            (one policy fold per term); default folds a body
+                            of 16 terms in plain double first */
+
+typedef struct pk_run_stats {
+  double kernel_ms;       /* device time of the call's kernels, max over devices */
+  double wall_ms;         /* host wall time spent inside the call */
+  uint64_t iterates;      /* Gray iterates walked */
+  uint64_t chunks;        /* aligned chunks walked by the register kernels */
+  uint64_t walker_ranges; /* unaligned pieces walked by the range walkers */
+  int32_t log2_chunk;     /* chunk size exponent k */
+  int32_t devices;        /* devices used */
+  int32_t launches;       /* kernel launches issued */
+  int32_t reserved;
+} pk_run_stats;
+
+int pk_abi_version(void);
+/* number of visible CUDA devices; < 0 on error */
+int pk_device_count(void);
+/* message for the last failing call on this thread ("" if none) */
+const char* pk_last_error(void);
+
+/* ---------------------------------------------------------------- dense real
+ * cols[j*n + i] = a_ij for j < n-1; x0[i] = a_{i,n-1} - rowsum_i / 2
+ * (dense_float_state, kernels.py:75-89).
+ *
+ * pk_dense_f64: one partial over iterates [start, end], reduced on the
+ * device(s) in a fixed tree order. Replaces run_range (parallel.py:232-289)
+ * for large ranges and the whole execute_plan + reduce_partials pipeline
+ * (parallel.py:318-387) when [start, end] = [1, 2^(n-1)-1].
+ * devices/ndev: CUDA device ordinals to spread the aligned chunks over
+ * (NULL/0 = device 0). log2_chunk: 0 = automatic.
+ */
+int pk_dense_f64(const double* cols, const double* x0, int n, uint64_t start, uint64_t end,
+                 int policy, uint32_t flags, int log2_chunk, const int* devices, int ndev,
+                 double out_dd[2], pk_run_stats* stats);
+
+/* nranges independent run_range partials, bit-identical to permkit's
+ * chunk_dense_f64 over each range (_loops.py:35-107). out: 2 doubles per range. */
+int pk_dense_f64_ranges(const double* cols, const double* x0, int n, const uint64_t* starts,
+                        const uint64_t* ends, int nranges, int policy, int device,
+                        double* out_dd);
+
+/* Per-chunk partials of the register kernel, for parity checks: chunks
+ * [chunk_lo, chunk_lo + nchunks) of size 2^log2_chunk (nchunks a multiple of
+ * 32), chunk c covering [1 + c*2^k, (c+1)*2^k] clipped to 2^(n-1)-1.
+ * out_chunks: 2 doubles per chunk; out_total: the device tree over them. */
+int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_chunk,
+                        uint64_t chunk_lo, uint64_t nchunks, int policy, uint32_t flags,
+                        int device, double* out_chunks, double out_total[2]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERMKIT_B200_H */

@@ -1,0 +1,272 @@
+// K1: dense real fp64 Gray walk over power-of-two aligned chunks.
+//
+// Replaces permkit's hot loop chunk_dense_f64 (/root/reference/pkg/src/permkit/
+// _loops.py:35-107) driven by run_range/init_x_at (parallel.py:162-188,
+// :232-289) over an aligned plan (parallel.py:95-122).
+//
+// Work unit: chunk c covers iterates [1 + c*2^k, (c+1)*2^k] -- the reference's
+// aligned chunk layout. Its state is jumped in at g_prev = c*2^k. Within the
+// chunk the changed column j = ctz(r) of local step r < 2^k is the same for
+// every chunk (the CEG property), so the walk is unrolled in
+// bodies of U = 2^LOGU steps whose U-1 inner steps have compile-time column
+// indices: their column entries are read straight out of the kernel-parameter
+// constant bank (DADD R, R, c[0x0][imm]) -- no load instruction at all. The
+// U-th step of each body flips a column >= LOGU chosen at run time (uniform
+// across the grid, read with LDC); the final step of the chunk flips a
+// chunk-specific column.
+//
+// x[N] is register resident (N is a template parameter). The product is a
+// sequential chain by default (PS = 1), which reproduces the reference's
+// rounding exactly; PS > 1 splits it into PS interleaved chains.
+#pragma once
+#include "pk_common.cuh"
+#include "pk_reduce.cuh"
+
+namespace pk {
+
+constexpr int kDenseBlock = 128;
+
+template <int N>
+struct DenseF64Params {
+  double cols[(N - 1) * N];  // cols[j*N + i] = a_ij for the n-1 toggled columns
+  double x0[N];              // a_{i,n-1} - rowsum_i / 2 (kernels.py:75-89)
+  dd_t* group_part;          // [num_groups] warp-tree partials
+  dd_t* chunk_part;          // optional [num_groups*32] per-chunk partials
+  dd_t* out;                 // launch total (tree over groups)
+  unsigned int* counter;     // last-block detector, zero on entry
+  unsigned long long chunk_lo;    // first chunk index of this launch
+  unsigned long long num_groups;  // groups of 32 consecutive chunks
+  unsigned long long g_end;       // inclusive last iterate of the walk
+  int k;                          // log2 chunk size, k > LOGU
+};
+
+__host__ __device__ constexpr int ctz_c(int q) {
+  int j = 0;
+  while (((q >> j) & 1) == 0) ++j;
+  return j;
+}
+
+template <int N, int PS>
+__device__ __forceinline__ double row_product(const double (&x)[N]) {
+  if constexpr (PS == 1) {
+    // prod = 1.0; prod *= x[i] (_loops.py:85-87); 1.0 * x[0] == x[0] exactly
+    double p = x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) p = __dmul_rn(p, x[i]);
+    return p;
+  } else {
+    double q[PS];
+#pragma unroll
+    for (int s = 0; s < PS; ++s) q[s] = (s < N) ? x[s] : 1.0;
+#pragma unroll
+    for (int i = PS; i < N; ++i) q[i % PS] = __dmul_rn(q[i % PS], x[i]);
+#pragma unroll
+    for (int w = 1; w < PS; w <<= 1)
+#pragma unroll
+      for (int s = 0; s + w < PS; s += 2 * w) q[s] = __dmul_rn(q[s], q[s + w]);
+    return q[0];
+  }
+}
+
+// Compile-time knobs of the walk:
+//   POL  accumulator policy of the per-chunk partial (pk_common.cuh)
+//   PS   product chains (1 = the reference's sequential product, bit exact)
+//   LOGU log2 of the unrolled body length U
+//   CS   where the static steps' column operands come from (below)
+//   BA   block accumulation: sum the U terms of a body in plain double and
+//        fold the body sum once (1 policy fold per U terms instead of per
+//        term). Not bit-identical to the reference's per-term fold.
+//   MINB minimum resident blocks per SM requested from ptxas (register cap)
+template <int POL_, int PS_, int LOGU_, int CS_, bool BA_, int MINB_ = 1>
+struct DenseCfg {
+  static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, CS = CS_, MINB = MINB_;
+  static constexpr bool BA = BA_ && POL_ != POL_QQ;
+};
+
+// Column-operand sources. Static steps index the columns with compile-time
+// offsets; what ptxas makes of that depends on whether it may hoist:
+//   CS_HOIST  -- plain indexing into the parameter block; ptxas hoists the
+//                body's columns into uniform + vector registers per chunk
+//   CS_RELOAD -- the index carries an opaque, loop-variant zero, so every
+//                body re-reads its columns from the constant bank (LDC)
+//   CS_SMEM   -- columns staged once per block in shared memory, read with
+//                warp-uniform LDS.128 (two doubles per load) every body
+enum ColSrc : int { CS_HOIST = 0, CS_RELOAD = 1, CS_SMEM = 2 };
+
+template <int N>
+__host__ __device__ constexpr int smem_stride() { return (N + 1) & ~1; }
+
+template <int N, class C>
+struct DenseWalk {
+  const DenseF64Params<N>& p;
+  const double* scols;  // shared-memory columns (CS_SMEM), stride smem_stride<N>()
+  double x[N];
+  Acc<C::POL> acc;
+  double bsum;
+
+  __device__ __forceinline__ DenseWalk(const DenseF64Params<N>& p_, const double* s_)
+      : p(p_), scols(s_) {}
+
+  // x[i] += sign * column entry, for a compile-time column J
+  template <int J, int SIGN>  // SIGN: +1, -1, or 0 (= runtime s)
+  __device__ __forceinline__ void update_static(int jz, double s) {
+    if constexpr (C::CS == CS_SMEM) {
+      constexpr int NP = smem_stride<N>();
+      const double2* c2 = reinterpret_cast<const double2*>(scols + (J + jz) * NP);
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const double2 v = c2[i / 2];
+        x[i] = apply<SIGN>(x[i], v.x, s);
+        if (i + 1 < N) x[i + 1] = apply<SIGN>(x[i + 1], v.y, s);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double c = (C::CS == CS_HOIST) ? p.cols[J * N + i] : p.cols[(J + jz) * N + i];
+        x[i] = apply<SIGN>(x[i], c, s);
+      }
+    }
+  }
+
+  template <int SIGN>
+  __device__ __forceinline__ static double apply(double xi, double c, double s) {
+    if constexpr (SIGN > 0) return __dadd_rn(xi, c);
+    else if constexpr (SIGN < 0) return __dsub_rn(xi, c);
+    else return __fma_rn(s, c, xi);  // s = +-1: x + s*c exactly as _loops.py:48
+  }
+
+  // runtime column j (uniform in the body's last step, per-chunk at the end)
+  __device__ __forceinline__ void update_dynamic(int j, double s) {
+    if constexpr (C::CS == CS_SMEM) {
+      constexpr int NP = smem_stride<N>();
+      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const double2 v = c2[i / 2];
+        x[i] = __fma_rn(s, v.x, x[i]);
+        if (i + 1 < N) x[i + 1] = __fma_rn(s, v.y, x[i + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = __fma_rn(s, p.cols[j * N + i], x[i]);
+    }
+  }
+
+  // fold the current state's signed product (term sign = iterate parity)
+  __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
+    if constexpr (C::POL == POL_QQ) {
+      double ph = 1.0, pl = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) qq_mul_step(ph, pl, x[i]);
+      if (odd) acc.sub2(ph, pl); else acc.add2(ph, pl);
+    } else {
+      const double pr = row_product<N, C::PS>(x);
+      if constexpr (C::BA) {
+        if (first_in_body) bsum = odd ? -pr : pr;
+        else bsum = odd ? __dsub_rn(bsum, pr) : __dadd_rn(bsum, pr);
+      } else {
+        if (odd) acc.sub(pr); else acc.add(pr);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void end_body() {
+    if constexpr (C::BA) acc.add(bsum);
+  }
+};
+
+// One compile-time step q (1 <= q < U) of a body: column J = ctz(q).
+template <int N, class C, int Q>
+__device__ __forceinline__ void static_step(DenseWalk<N, C>& w, double s_mid, int jz) {
+  constexpr int J = ctz_c(Q);
+  if constexpr (J + 1 < C::LOGU) {
+    // direction from bit J+1 of the local index: compile time
+    w.template update_static<J, (((Q >> (J + 1)) & 1) == 0) ? 1 : -1>(jz, 0.0);
+  } else {
+    // J == LOGU-1: direction from bit LOGU of g, fixed per body
+    w.template update_static<J, 0>(jz, s_mid);
+  }
+  // iterate parity == local parity (chunk bases are even): odd -> subtract
+  w.fold((Q & 1) != 0, Q == 1);
+}
+
+template <int N, class C, int Q, int U>
+struct StaticSteps {
+  __device__ __forceinline__ static void run(DenseWalk<N, C>& w, double s_mid, int jz) {
+    static_step<N, C, Q>(w, s_mid, jz);
+    StaticSteps<N, C, Q + 1, U>::run(w, s_mid, jz);
+  }
+};
+template <int N, class C, int U>
+struct StaticSteps<N, C, U, U> {
+  __device__ __forceinline__ static void run(DenseWalk<N, C>&, double, int) {}
+};
+
+// Walk one aligned chunk; returns its normalised partial (parallel.py:282-289).
+template <int N, class C>
+__device__ __forceinline__ dd_t walk_chunk(const DenseF64Params<N>& p, const double* scols,
+                                           uint64_t c) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  DenseWalk<N, C> w(p, scols);
+  const int k = p.k;
+  const uint64_t base = c << k;
+#pragma unroll
+  for (int i = 0; i < N; ++i) w.x[i] = p.x0[i];
+  // jump-in (init_x_at, parallel.py:162-188): x0 + columns of gray(base), ascending
+  const uint64_t code = base ^ (base >> 1);
+  for (int j = 0; j < N - 1; ++j) {
+    if ((code >> j) & 1ull) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) w.x[i] = __dadd_rn(w.x[i], p.cols[j * N + i]);
+    }
+  }
+  const uint64_t nbody = 1ull << (k - LOGU);
+  for (uint64_t m = 0; m < nbody; ++m) {
+    const uint64_t gb = base + (m << LOGU);
+    const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
+    const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
+    StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
+    // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
+    const uint64_t g = gb + U;
+    if (m + 1 < nbody || g <= p.g_end) {
+      const int j = changed_col(g);
+      w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
+      w.fold(false, false);
+    }
+    w.end_body();
+  }
+  return w.acc.partial();
+}
+
+template <int N, class C>
+__global__ void __launch_bounds__(kDenseBlock, C::MINB)
+    dense_f64_chunks(const __grid_constant__ DenseF64Params<N> p) {
+  extern __shared__ __align__(16) double scols[];
+  if constexpr (C::CS == CS_SMEM) {
+    constexpr int NP = smem_stride<N>();
+    for (int t = threadIdx.x; t < (N - 1) * NP; t += blockDim.x) {
+      const int j = t / NP, i = t % NP;
+      scols[t] = (i < N) ? p.cols[j * N + i] : 0.0;
+    }
+    __syncthreads();
+  }
+  const unsigned int lane = threadIdx.x & 31u;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
+    const uint64_t c = p.chunk_lo + grp * 32 + lane;
+    dd_t part = walk_chunk<N, C>(p, scols, c);
+    if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
+    part = warp_tree_dd(part);
+    if (lane == 0) p.group_part[grp] = part;
+  }
+  grid_tail_reduce<kDenseBlock>(p.group_part, p.num_groups, p.out, p.counter);
+}
+
+template <int N, class C>
+__host__ __device__ constexpr size_t dense_smem_bytes() {
+  return C::CS == CS_SMEM ? sizeof(double) * (N - 1) * smem_stride<N>() : 0;
+}
+
+}  // namespace pk

@@ -1,0 +1,71 @@
+// Host-side launcher template for the N-specialised dense real kernel.
+// Included by the pk_dense_f64_n*.cu units, each instantiating a range of N.
+#pragma once
+#include <cstring>
+
+#include "pk_dense_f64.cuh"
+#include "pk_launch.h"
+
+namespace pk {
+
+template <int N, class C>
+static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
+  auto kern = dense_f64_chunks<N, C>;
+  constexpr size_t smem = dense_smem_bytes<N, C>();
+  static int occ = -1;  // per instantiation; every B200 gives the same answer
+  if (occ < 0) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kDenseBlock, smem);
+    if (e != cudaSuccess) return (int)e;
+    occ = o > 0 ? o : 1;
+  }
+  const uint64_t warps_needed = a.num_groups;
+  const uint64_t blocks_needed = (warps_needed * 32 + kDenseBlock - 1) / kDenseBlock;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if (blocks_needed < grid) grid = blocks_needed;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kDenseBlock, smem, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_dense_f64(const DenseLaunch& a) {
+  static_assert(N >= kDenseNMin && N <= kDenseNMax, "order out of range");
+  constexpr int LOGU = dense_logu(N);
+  constexpr int MB = dense_minb(N);
+  DenseF64Params<N> p;
+  std::memcpy(p.cols, a.cols, sizeof(double) * (N - 1) * N);
+  std::memcpy(p.x0, a.x0, sizeof(double) * N);
+  p.group_part = a.group_part;
+  p.chunk_part = a.chunk_part;
+  p.out = a.out;
+  p.counter = a.counter;
+  p.chunk_lo = a.chunk_lo;
+  p.num_groups = a.num_groups;
+  p.g_end = a.g_end;
+  p.k = a.k;
+  switch (a.policy) {
+    case POL_DD:
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+    case POL_KAHAN:
+      return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+    case POL_DQ:
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+    case POL_QQ:
+      return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, CS_SMEM, false, MB>>(a, p);
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pk
+
+#define PK_INSTANTIATE_DENSE_F64(N) template int pk::launch_dense_f64<N>(const pk::DenseLaunch&);

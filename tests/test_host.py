@@ -1,0 +1,166 @@
+"""Host-side logic that needs no GPU: the C-ABI library loads and exports
+every symbol the public header declares; plans, containers, precision and
+the partial-result reduction behave like the reference's
+(/root/reference/pkg/tests/test_parallel.py, test_matrix.py,
+test_precision.py)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2502_16577_b200 as pk
+from paper_2502_16577_b200 import _native
+from paper_2502_16577_b200.parallel import PartialResult
+from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_pairwise
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "permkit_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pk_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.load()
+    syms = header_symbols()
+    assert "pk_dense_f64" in syms and len(syms) >= 6
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _native.SIGNATURES, f"{s} lacks a ctypes signature"
+    assert lib.pk_abi_version() == 1
+
+
+def test_no_device_is_a_loud_error():
+    # CPU container: the call must fail with DeviceError, never compute on the host
+    try:
+        if _native.device_count() > 0:
+            pytest.skip("a GPU is visible")
+    except pk.DeviceError:
+        pass
+    with pytest.raises(pk.DeviceError):
+        pk.perm_nw(pk.random_real(12, 1))
+
+
+def test_plan_tiling_and_alignment():
+    for n in range(2, 21):
+        for tau in (1, 2, 3, 7, 16, 64):
+            for aligned in (True, False):
+                plan = pk.plan_chunks(n, tau, aligned)
+                spans = list(plan.ranges) + ([plan.residual] if plan.residual else [])
+                pos = 1
+                for (s, e) in spans:
+                    assert s == pos and e >= s
+                    pos = e + 1
+                assert pos == pk.total_iterates(n) + 1
+                if aligned and plan.chunk_size:
+                    assert plan.chunk_size & (plan.chunk_size - 1) == 0
+    assert pk.plan_chunks(3, 100).tau_clamped
+    with pytest.raises(ValueError):
+        pk.plan_chunks(64, 4)
+    with pytest.raises(ValueError):
+        pk.plan_chunks(8, 0)
+
+
+def test_alignment_report():
+    for n in (10, 12, 14):
+        for tau in (2, 4, 8):
+            counts = pk.cbl_alignment_report(pk.plan_chunks(n, tau, aligned=True))
+            assert all(c == 1 for c in counts[:-1])
+    assert max(pk.cbl_alignment_report(pk.fixed_chunk_plan(12, 17, 4))) >= 3
+
+
+def test_hierarchy_flattens_like_reference():
+    for n in range(6, 15):
+        for p in range(1, 5):
+            for w in range(1, 4):
+                h = pk.plan_hierarchy(n, p, w, aligned=False)
+                flat = h.flatten()
+                assert [x[0] for x in flat] == list(range(len(flat)))
+                got = []
+                for pi in range(h.processes):
+                    got.extend(h.jobs_for(pi))
+                assert got == flat
+    with pytest.raises(ValueError):
+        pk.plan_hierarchy(3, 4, 4)
+
+
+def test_graycode():
+    assert pk.cbl_sequence(3) == [0, 1, 0, 2, 0, 1, 0]
+    for g in range(1, 1 << 12):
+        st = pk.changed_bit(g)
+        assert pk.gray_of(g) ^ pk.gray_of(g - 1) == 1 << st.j
+        assert st.s == (1 if (pk.gray_of(g) >> st.j) & 1 else -1)
+
+
+def test_containers_and_kinds():
+    m = pk.DenseMatrix.from_rows([[1, 2], [3, 4]])
+    assert m.kind == "integer"
+    assert pk.DenseMatrix.from_rows([[1.0, 2], [3, 4]]).kind == "real64"
+    assert pk.DenseMatrix.from_rows([[1j, 2], [3, 4]]).kind == "complex128"
+    with pytest.raises(pk.ImpossibleError):
+        pk.DenseMatrix.from_rows([[1] * 64 for _ in range(64)])
+    with pytest.raises(pk.StructureError):
+        pk.DenseMatrix.from_rows([[1, 2]])
+    with pytest.raises(pk.StructureError):
+        pk.DenseMatrix.from_rows([[float("nan")]])
+    s = pk.dense_to_sparse(pk.DenseMatrix.from_rows([[0, 2], [3, 0]]))
+    assert s.nnz == 2 and s.ccs.cptrs == (0, 1, 2) and s.ccs.rids == (1, 0)
+    s.validate()
+    assert pk.sparse_to_dense(s).rows() == [[0, 2], [3, 0]]
+    with pytest.raises(pk.StructureError):
+        pk.sparse_from_triplets(2, [(0, 0, 1), (0, 0, 2)], "integer")
+
+
+def test_reference_objects_are_accepted():
+    class Fake:
+        n = 2
+        kind = "real64"
+        data = (1.0, 2.0, 3.0, 4.0)
+    m = pk.coerce_matrix(Fake())
+    assert isinstance(m, pk.DenseMatrix) and m.entry(1, 0) == 3.0
+
+
+def test_policy_parse_and_codes():
+    assert AccumulatorPolicy.parse("KAHAN") is AccumulatorPolicy.KAHAN
+    assert [p.code for p in AccumulatorPolicy] == [0, 1, 2, 3]
+    with pytest.raises(ValueError):
+        AccumulatorPolicy.parse("fast")
+
+
+def test_dd_pairwise_is_balanced_tree():
+    vals = [DoubleDouble(float(i) * 1e-3 + 1.0, 0.0) for i in range(8)]
+    t = dd_pairwise(vals)
+    l = pk.dd_add(pk.dd_add(vals[0], vals[1]), pk.dd_add(vals[2], vals[3]))
+    r = pk.dd_add(pk.dd_add(vals[4], vals[5]), pk.dd_add(vals[6], vals[7]))
+    assert t == pk.dd_add(l, r)
+
+
+def test_reduce_partials_validation():
+    n = 6
+    parts = [PartialResult(0, 1, 16, 16, "real64", DoubleDouble(1.0, 0.0)),
+             PartialResult(1, 17, 31, 15, "real64", DoubleDouble(2.0, 0.0))]
+    assert pk.reduce_partials(parts, 0.5, n) == -7.0
+    assert pk.reduce_partials(list(reversed(parts)), 0.5, n) == -7.0
+    with pytest.raises(pk.StructureError):
+        pk.reduce_partials(parts[1:], 0.5, n)
+    with pytest.raises(pk.StructureError):
+        pk.reduce_partials(parts + [parts[0]], 0.5, n)
+
+
+def test_partials_file_round_trip(tmp_path):
+    m = pk.random_real(6, 3)
+    parts = [PartialResult(0, 1, 16, 16, "real64", DoubleDouble(1.25, 2.0 ** -60)),
+             PartialResult(1, 17, 31, 15, "real64", DoubleDouble(-2.0, 0.0))]
+    path = tmp_path / "p.txt"
+    pk.write_partials_file(path, m, "dd", parts)
+    header, got = pk.read_partials_file(path)
+    assert header["n"] == 6 and got == parts
+    assert header["matrix_sha256"] == pk.matrix_content_hash(m)
+    assert pk.matrix_content_hash(m) == pk.matrix_content_hash(pk.dense_to_sparse(m))
+    bad = tmp_path / "bad.txt"
+    bad.write_text("# nope\n" + path.read_text())
+    with pytest.raises(pk.ParseError):
+        pk.read_partials_file(bad)
