@@ -1,0 +1,420 @@
+"""Benchmark: Gray-code updates/s of the dense real fp64 permanent walk.
+
+Workload (BASELINE.json metric "Gray-code updates/sec & wall time, n=40/48
+dense fp64, 1/2/4/8 B200 vs FP64 peak"): one step = the whole Gray walk of a
+40x40 random [0,1) matrix (seed 20261017, policy KAHAN), 2^39 - 1 updates,
+split over the N GPUs as contiguous power-of-two iterate ranges (strong
+scaling: total work fixed). Each rank walks its range on its GPU; rank 0
+combines the N double-double partials in fixed rank order.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 40] [--policy kahan]
+    python bench.py --impl reference ...   # the reference's CPU path on host cores
+
+Timing: W untimed steps, then K timed steps, each bracketed by a barrier and
+device synchronisation. `value` uses the CUDA-event time of the walk kernels
+on their launch stream (max over ranks, summed over steps); `e2e` the wall
+time of the public API call permanent() from a host matrix (H2D of the
+inputs and D2H of the result inside), max over ranks. L2 is flushed between
+steps (the inputs are 12.8 KB; the walk is FP64-pipe bound).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+SEED = 20261017
+ROOT = os.path.dirname(os.path.abspath(__file__))
+METRIC = "Gray-code updates/sec & wall time, n=40/48 dense fp64, 1/2/4/8 B200 vs FP64 peak"
+# SUperman x_reg-A_shr-rebuild + CEG on a Quadro GV100, n=40: 14.17 s
+PAPER_N40_UPS = ((1 << 39) - 1) / 14.17
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=40)
+    ap.add_argument("--policy", default="kahan")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-log2", type=int, default=31,
+                    help="iterates of the n-walk timed for the CPU baseline (2^x)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (one process per GPU; torch.distributed over NCCL)
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def gather_f64(self, vals):
+        """all ranks' float lists -> list per rank (rank order)."""
+        if not self.pg:
+            return [list(vals)]
+        import torch
+        t = torch.tensor(list(vals), dtype=torch.float64, device=f"cuda:{self.local}")
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.pg.all_gather(out, t)
+        return [o.cpu().tolist() for o in out]
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def sync_device():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    except Exception:
+        pass
+
+
+# ---------------------------------------------------------------------------
+# clocks and L2 flush
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+class L2Flusher:
+    def __init__(self, local: int):
+        self.buf = None
+        try:
+            import torch
+            self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+        except Exception:
+            self.buf = None
+
+    def flush(self):
+        if self.buf is not None:
+            self.buf.zero_()
+            sync_device()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own CPU path, bounded sample
+
+
+def _reference_importable():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "permkit")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/pk_numba_cache")
+        try:
+            import permkit  # noqa: F401
+            from permkit import _loops
+            return bool(_loops.HAVE_NUMBA)
+        except Exception:
+            return False
+    return False
+
+
+def cpu_updates_per_s(n: int, policy: str, sample_log2: int, rows):
+    """Time the reference CPU implementation on a bounded, contiguous sample
+    of the n-walk (2^sample_log2 iterates from g=1) split over all host
+    cores. Uses permkit itself (numba JIT, execute_plan's thread-pool
+    mechanism) when baseline/_ref is present, else the oracle C port."""
+    cores = os.cpu_count() or 1
+    total = (1 << (n - 1)) - 1
+    count = min(1 << sample_log2, total)
+    nchunks = 8 * cores
+    size = max(1, count // nchunks)
+    spans = [(1 + i * size, (i + 1) * size) for i in range(nchunks)]
+    updates = size * nchunks
+    if _reference_importable():
+        from concurrent.futures import ThreadPoolExecutor
+        import permkit
+        from permkit.parallel import run_range
+        from permkit.precision import AccumulatorPolicy
+        pol = AccumulatorPolicy.parse(policy)
+        m = permkit.DenseMatrix.from_rows(rows)
+        run_range(m, 1, 1024, pol)  # JIT warm-up
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            list(ex.map(lambda se: run_range(m, se[0], se[1], pol), spans))
+        dt = time.perf_counter() - t0
+        kind = "reference"
+        how = "permkit.parallel.run_range (numba) on a thread pool, as execute_plan"
+    else:
+        sys.path.insert(0, ROOT)
+        import oracle
+        a = np.array(rows, dtype=np.float64)
+        t0 = time.perf_counter()
+        oracle.dense_f64_ranges_mt(a, spans, policy, cores)
+        dt = time.perf_counter() - t0
+        kind = "port"
+        how = "oracle/permref.c restatement, pthreads"
+    return {"value": updates / dt, "unit": "updates/s", "cores": cores, "kind": kind,
+            "sample": f"iterates [1, {updates}] of the n={n} walk ({how}), {dt:.2f} s"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def matrix_rows(n):
+    g = np.random.default_rng(SEED).uniform(0.0, 1.0, size=(n, n))
+    return [[float(v) for v in r] for r in g]
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return 0
+    rows = matrix_rows(args.n)
+    samples = []
+    log2 = min(args.cpu_sample_log2 - 2, args.n - 2)
+    for i in range(args.warmup + args.steps):
+        r = cpu_updates_per_s(args.n, args.policy, log2, rows)
+        if i >= args.warmup:
+            samples.append(r)
+    ups = statistics.median(s["value"] for s in samples)
+    total = (1 << (args.n - 1)) - 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ups, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / ups * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": ups / PAPER_N40_UPS, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"n={args.n} dense real fp64 random [0,1) seed {SEED}, "
+                               f"policy {args.policy}; per step a bounded sample of the walk "
+                               f"on the host cores (extrapolated ms_per_step)",
+                   "n": args.n, "policy": args.policy},
+        "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {"value": ups,
+                                                                                    "unit": "updates/s"},
+        "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, dist: Dist):
+    sys.path.insert(0, ROOT)
+    import paper_2502_16577_b200 as pk
+    from paper_2502_16577_b200 import _native
+    from paper_2502_16577_b200.kernels import DenseF64Problem, policy_product, _sign_factor
+    from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_add, dd_pairwise
+
+    n, N, rank = args.n, dist.world, dist.rank
+    pol = AccumulatorPolicy.parse(args.policy)
+    rows = matrix_rows(n)
+    m = pk.DenseMatrix.from_rows(rows)
+    total = (1 << (n - 1)) - 1
+    span = (1 << (n - 1)) // N
+    lo, hi = rank * span + 1, min((rank + 1) * span, total)
+    dev = [dist.local]
+    flusher = L2Flusher(dist.local)
+
+    def step_device():
+        st = _native.RunStats()
+        prob = DenseF64Problem(m)  # host marshalling is part of every call
+        part = prob.walk(lo, hi, pol, devices=dev, stats=st)
+        return part, st
+
+    def step_e2e():
+        # the public API path, host matrix in, host scalar out
+        t0 = time.perf_counter()
+        if N == 1:
+            v = pk.permanent(rows, args.policy)
+        else:
+            part, _ = step_device()
+            v = part
+        return v, (time.perf_counter() - t0) * 1e3
+
+    for _ in range(args.warmup):
+        step_device()
+        step_e2e()
+    sync_device()
+
+    peak_tf = _native.fp64_peak_tflops(dist.local)
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    kernel_ms, wall_ms, launches, parts = [], [], 0, []
+    for _ in range(args.steps):
+        flusher.flush()
+        dist.barrier()
+        sync_device()
+        t0 = time.perf_counter()
+        part, st = step_device()
+        sync_device()
+        w = (time.perf_counter() - t0) * 1e3
+        dist.barrier()
+        kernel_ms.append(st.kernel_ms)
+        wall_ms.append(w)
+        launches += st.launches
+        parts.append(part)
+        k_used = st.log2_chunk
+    e2e_ms = []
+    for _ in range(args.steps):
+        flusher.flush()
+        dist.barrier()
+        sync_device()
+        _, w = step_e2e()
+        sync_device()
+        dist.barrier()
+        e2e_ms.append(w)
+    clocks.stop()
+
+    # max over ranks, per step
+    g_k = dist.gather_f64(kernel_ms)
+    g_w = dist.gather_f64(wall_ms)
+    g_e = dist.gather_f64(e2e_ms)
+    g_part = dist.gather_f64([parts[-1].hi, parts[-1].lo])
+    g_launch = dist.gather_f64([float(launches)])
+    if rank != 0:
+        return 0
+    step_k = [max(g[i] for g in g_k) for i in range(args.steps)]
+    step_w = [max(g[i] for g in g_w) for i in range(args.steps)]
+    step_e = [max(g[i] for g in g_e) for i in range(args.steps)]
+    ups = args.steps * total / (sum(step_k) * 1e-3)
+    e2e_ups = args.steps * total / (sum(step_e) * 1e-3)
+
+    # fixed-order host reduction of the per-GPU partials (+ the g = 0 term)
+    x0 = DenseF64Problem(m).x0
+    p0 = policy_product(x0, pol)
+    acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+    acc = dd_add(acc, dd_pairwise([tuple(g) for g in g_part]))
+    perm = acc.hi * _sign_factor(n)
+
+    flops_per_update = 3 * n
+    # per launch: one walk kernel per GPU per step, timed with CUDA events
+    achieved_tf = flops_per_update * (total / N) / (statistics.mean(step_k) * 1e-3) * 1e-12
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    cpu = None
+    if not args.no_cpu_baseline and N == 1:
+        cpu = cpu_updates_per_s(n, args.policy, args.cpu_sample_log2, rows)
+    input_bytes = (n - 1) * n * 8 + n * 8
+    line = {
+        "metric": METRIC,
+        "value": ups,
+        "unit": "updates/s",
+        "n_gpus": N,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": statistics.mean(step_k),
+        "wall_ms_per_step": statistics.mean(step_w),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": ups / PAPER_N40_UPS if n == 40 else None,
+        "vs_baseline_ref": "SUperman best kernel on a Quadro GV100, n=40 in 14.17 s "
+                           "(PAPER.md:785) = 3.88e10 updates/s",
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"n={n} dense real fp64 permanent, random [0,1) seed {SEED}, "
+                               f"policy {args.policy}, whole Gray walk (2^{n - 1}-1 updates) "
+                               f"per step", "n": n, "policy": args.policy,
+                   "split": f"{N} contiguous power-of-two iterate ranges, one per GPU",
+                   "log2_chunk": k_used, "l2": "flushed (256 MiB write) between steps",
+                   "permanent": perm.hex()},
+        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+                     "traffic": None,
+                     "note": f"algorithmic {flops_per_update} flop/update (n DFMA-equivalent adds, "
+                             "n-1 DMUL, 1 accumulate) x updates per launch / event time; peak = "
+                             "live DFMA microbenchmark (pk_fp64_peak; MEASURED_PEAKS.json has no "
+                             "FP64 entry, hbm_gbs=%s bf16=%s)" % (peaks.get("hbm_gbs"),
+                                                                  peaks.get("bf16_tflops"))},
+        "e2e": {"value": e2e_ups, "unit": "updates/s",
+                "h2d_bytes_per_step": 2 * input_bytes * N, "d2h_bytes_per_step": 16 * N,
+                "ms_per_step": statistics.mean(step_e),
+                "path": "paper_2502_16577_b200.permanent(rows) (N=1) / walk(range) per rank"},
+        "gpu_launches": int(sum(g[0] for g in g_launch)),
+        "clocks": clocks.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            return run_reference(args, dist)
+        return run_b200(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

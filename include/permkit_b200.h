@@ -72,6 +72,11 @@ int pk_device_count(void);
 /* message for the last failing call on this thread ("" if none) */
 const char* pk_last_error(void);
 
+/* measured FP64 peak (DFMA chains, 2 flops each) of `device` in TFLOP/s: the
+ * roofline denominator of the FP64-bound walk kernels. iters ~ 20000 gives a
+ * ~40 ms measurement on a B200. */
+int pk_fp64_peak(int device, int iters, double* tflops, double* ms);
+
 /* ---------------------------------------------------------------- dense real
  * cols[j*n + i] = a_ij for j < n-1; x0[i] = a_{i,n-1} - rowsum_i / 2
  * (dense_float_state, kernels.py:75-89).
@@ -100,6 +105,27 @@ int pk_dense_f64_ranges(const double* cols, const double* x0, int n, const uint6
 int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_chunk,
                         uint64_t chunk_lo, uint64_t nchunks, int policy, uint32_t flags,
                         int device, double* out_chunks, double out_total[2]);
+
+/* ------------------------------------------------------------- dense complex
+ * Interleaved (re, im) doubles: cols[2*(j*n + i) + {0,1}] = a_ij (j < n-1),
+ * x0[2*i + {0,1}] = a_{i,n-1} - rowsum_i / 2 (dense_complex_state,
+ * kernels.py:92-101). Complex runs use the plain-double policy only
+ * (kernels.py:309-310); the register kernels keep (re, im) partials per
+ * chunk and reduce each component as a double-double tree.
+ *
+ * pk_dense_c128: out = (re_hi, re_lo, im_hi, im_lo) over [start, end]
+ * (register kernels for 11 <= n <= 40, range walkers otherwise).
+ * pk_dense_c128_ranges: bit-identical run_range partials, out = (re, im) per
+ * range (chunk_dense_c128, _loops.py:186-209).
+ * pk_dense_c128_chunks: per-chunk (re, im) partials, out_total as above. */
+int pk_dense_c128(const double* cols, const double* x0, int n, uint64_t start, uint64_t end,
+                  uint32_t flags, int log2_chunk, const int* devices, int ndev, double out[4],
+                  pk_run_stats* stats);
+int pk_dense_c128_ranges(const double* cols, const double* x0, int n, const uint64_t* starts,
+                         const uint64_t* ends, int nranges, int device, double* out);
+int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_chunk,
+                         uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
+                         double* out_chunks, double out_total[4]);
 
 #ifdef __cplusplus
 }

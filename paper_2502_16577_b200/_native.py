@@ -64,6 +64,7 @@ SIGNATURES = {
     "pk_abi_version": (ctypes.c_int, []),
     "pk_device_count": (ctypes.c_int, []),
     "pk_last_error": (ctypes.c_char_p, []),
+    "pk_fp64_peak": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, _D]),
     "pk_dense_f64": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.c_int, ctypes.c_uint32, ctypes.c_int, _I32, ctypes.c_int,
                                     _D, ctypes.POINTER(RunStats)]),
@@ -72,6 +73,14 @@ SIGNATURES = {
     "pk_dense_f64_chunks": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                            ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32,
                                            ctypes.c_int, _D, _D]),
+    "pk_dense_c128": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                     ctypes.c_uint32, ctypes.c_int, _I32, ctypes.c_int, _D,
+                                     ctypes.POINTER(RunStats)]),
+    "pk_dense_c128_ranges": (ctypes.c_int, [_D, _D, ctypes.c_int, _U64, _U64, ctypes.c_int,
+                                            ctypes.c_int, _D]),
+    "pk_dense_c128_chunks": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                            ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _D,
+                                            _D]),
 }
 
 
@@ -125,6 +134,15 @@ def device_count() -> int:
     if c < 0:
         raise DeviceError("cudaGetDeviceCount failed")
     return c
+
+
+def fp64_peak_tflops(device: int = 0, iters: int = 20000) -> float:
+    """Live DFMA throughput of `device` (the FP64 roofline denominator)."""
+    tf = ctypes.c_double(0.0)
+    ms = ctypes.c_double(0.0)
+    rc = load().pk_fp64_peak(device, iters, ctypes.byref(tf), ctypes.byref(ms))
+    check(rc, "pk_fp64_peak")
+    return tf.value
 
 
 def dptr(a: np.ndarray):

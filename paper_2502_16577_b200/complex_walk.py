@@ -1,9 +1,108 @@
-"""Complex walk (placeholder until the c128 kernels land)."""
+"""Complex (boson-sampling) walks on the GPU: dense complex register kernels
+(csrc/pk_dense_c128.cuh, 11 <= n <= 40) and complex range walkers.
+
+Sparse complex pairs run as their densified twin with the sparse seed: the
+dense walk adds s*0 for absent entries, which leaves x unchanged, so the
+arithmetic is the reference's sparse loop (_loops.py:212-235).
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as nat
+from .kernels import _sign_factor, dense_complex_state, sparse_complex_state, total_iterates
+from .matrix import DenseMatrix, SparsePair, sparse_to_dense
+from .precision import DoubleDouble, dd_add
 
 
-def complex_walk_total(m, devices=None):
-    raise NotImplementedError("complex kernels not built yet")
+class DenseC128Problem:
+    def __init__(self, m):
+        if isinstance(m, SparsePair):
+            dense = sparse_to_dense(m)
+            cols, _ = dense_complex_state(dense)
+            x0 = sparse_complex_state(m)[3]
+            self.n = m.n
+        else:
+            cols, x0 = dense_complex_state(m)
+            self.n = m.n
+        c = np.ascontiguousarray(cols, dtype=np.complex128).reshape(-1)
+        self.cols = np.ascontiguousarray(c.view(np.float64)) if c.size else np.zeros(2)
+        self.x0c = np.ascontiguousarray(x0, dtype=np.complex128)
+        self.x0 = np.ascontiguousarray(self.x0c.view(np.float64))
+
+    def walk(self, start: int, end: int, *, exact: bool = False,
+             devices: Optional[Sequence[int]] = None, log2_chunk: int = 0,
+             stats: Optional[nat.RunStats] = None) -> Tuple[DoubleDouble, DoubleDouble]:
+        lib = nat.load()
+        out = np.zeros(4)
+        dptr, nd, _keep = nat.devices_arg(devices)
+        st = stats if stats is not None else nat.RunStats()
+        rc = lib.pk_dense_c128(nat.dptr(self.cols), nat.dptr(self.x0), self.n, start, end,
+                               nat.PK_FLAG_EXACT if exact else 0, log2_chunk, dptr, nd,
+                               nat.dptr(out), st)
+        nat.check(rc, "pk_dense_c128")
+        return DoubleDouble(out[0], out[1]), DoubleDouble(out[2], out[3])
+
+    def ranges(self, spans: Sequence[Tuple[int, int]], device: int = 0) -> List[complex]:
+        if not spans:
+            return []
+        lib = nat.load()
+        s = np.ascontiguousarray(np.array([a for a, _ in spans], dtype=np.uint64))
+        e = np.ascontiguousarray(np.array([b for _, b in spans], dtype=np.uint64))
+        out = np.zeros(2 * len(spans))
+        rc = lib.pk_dense_c128_ranges(nat.dptr(self.cols), nat.dptr(self.x0), self.n,
+                                      nat.u64ptr(s), nat.u64ptr(e), len(spans), device,
+                                      nat.dptr(out))
+        nat.check(rc, "pk_dense_c128_ranges")
+        return [complex(out[2 * i], out[2 * i + 1]) for i in range(len(spans))]
+
+    def chunks(self, log2_chunk: int, chunk_lo: int, nchunks: int, exact: bool = True,
+               device: int = 0):
+        lib = nat.load()
+        out = np.zeros(2 * nchunks)
+        tot = np.zeros(4)
+        rc = lib.pk_dense_c128_chunks(nat.dptr(self.cols), nat.dptr(self.x0), self.n, log2_chunk,
+                                      chunk_lo, nchunks, nat.PK_FLAG_EXACT if exact else 0,
+                                      device, nat.dptr(out), nat.dptr(tot))
+        nat.check(rc, "pk_dense_c128_chunks")
+        return out.reshape(-1, 2), (DoubleDouble(tot[0], tot[1]), DoubleDouble(tot[2], tot[3]))
+
+    def p0(self) -> complex:
+        p = complex(1.0)
+        for v in self.x0c:
+            p = p * complex(v)
+        return p
 
 
-def complex_ranges(m, spans, exact=None, devices=None):
-    raise NotImplementedError("complex kernels not built yet")
+def complex_walk_total(m, devices=None, stats=None) -> complex:
+    prob = DenseC128Problem(m)
+    n = prob.n
+    p0 = prob.p0()
+    re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+    if n > 1:
+        wr, wi = prob.walk(1, total_iterates(n), devices=devices, stats=stats)
+        re, im = dd_add(re, wr), dd_add(im, wi)
+    sign = _sign_factor(n)
+    return complex(re.hi * sign, im.hi * sign)
+
+
+EXACT_RANGE_LIMIT = 1 << 22
+
+
+def complex_ranges(m, spans, exact=None, devices=None) -> List[complex]:
+    prob = DenseC128Problem(m)
+    dev0 = devices[0] if devices else 0
+    out: List[Optional[complex]] = [None] * len(spans)
+    small = [i for i, (s, e) in enumerate(spans)
+             if exact is True or (exact is None and e - s + 1 <= EXACT_RANGE_LIMIT)]
+    if small:
+        for i, v in zip(small, prob.ranges([spans[i] for i in small], device=dev0)):
+            out[i] = v
+    for i, (s, e) in enumerate(spans):
+        if out[i] is None:
+            wr, wi = prob.walk(s, e, devices=devices)
+            out[i] = complex(wr.hi + wr.lo, wi.hi + wi.lo)
+    return out

@@ -17,6 +17,7 @@
 #include "permkit_b200.h"
 #include "pk_launch.h"
 #include "pk_walker.cuh"
+#include <functional>
 
 namespace {
 
@@ -201,11 +202,10 @@ struct DensePlan {
   std::vector<Range> head, tail;
 };
 
-DensePlan plan_dense(int n, uint64_t start, uint64_t end, int log2_chunk, int ndev) {
+DensePlan plan_dense(int n, int logu, uint64_t start, uint64_t end, int log2_chunk, int ndev) {
   DensePlan pl;
   const uint64_t len = end - start + 1;
-  if (n >= pk::kDenseNMin) {
-    const int logu = pk::dense_logu(n);
+  if (logu > 0) {
     int k = log2_chunk;
     if (k <= 0) {
       k = bit_length(len) - 22;
@@ -240,7 +240,28 @@ DensePlan plan_dense(int n, uint64_t start, uint64_t end, int log2_chunk, int nd
 }
 
 // ---------------------------------------------------------------------------
-// dense real
+// kinds: each bundles its device inputs, its register-kernel launcher and
+// its walker launcher; the driver below is shared.
+
+struct Kind {
+  int n = 0;
+  int streams = 1;            // double-double streams per partial: 1 real, 2 complex
+  int logu = 0;               // body length of the register kernel; 0 = walkers only
+  std::vector<double> input;  // uploaded once per device call: cols then x0
+  // register kernel over groups [chunk_lo, chunk_lo + 32*groups); returns cudaError_t
+  std::function<int(DevCtx&, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                    uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out)>
+      fast;
+  // walkers: one thread per range, out[r] = range partial
+  std::function<void(DevCtx&, const double* d_in, const unsigned long long* d_s,
+                     const unsigned long long* d_e, int nr, dd_t* out)>
+      walk;
+  // walker partial -> per-stream double-double
+  dd_t stream_of(const dd_t& w, int s) const {
+    if (streams == 1) return w;
+    return dd_t{s == 0 ? w.hi : w.lo, 0.0};
+  }
+};
 
 int dispatch_dense(int n, const pk::DenseLaunch& a) {
   switch (n) {
@@ -261,109 +282,185 @@ int dispatch_dense(int n, const pk::DenseLaunch& a) {
   }
 }
 
-struct DenseInputs {
-  const double* cols;
-  const double* x0;
-  int n;
-  int policy;
-  bool exact;
-};
-
-// walker launch for a list of ranges on ctx (workspace laid out in scratch)
-void launch_walk_dense(DevCtx& c, const DenseInputs& in, const std::vector<Range>& ranges,
-                       dd_t* d_out) {
-  const int n = in.n;
-  const size_t ncol = (size_t)(n > 1 ? n - 1 : 1) * n;
-  const size_t nr = ranges.size();
-  const size_t bytes = ncol * 8 + (size_t)n * 8 + nr * 16;
-  ensure(c.scratch, c.scratch_cap, bytes + 64);
-  char* base = c.scratch;
-  double* d_cols = (double*)base;
-  double* d_x0 = d_cols + ncol;
-  unsigned long long* d_s = (unsigned long long*)(d_x0 + n);
-  unsigned long long* d_e = d_s + nr;
-  std::vector<unsigned long long> hs(nr), he(nr);
-  for (size_t i = 0; i < nr; ++i) {
-    hs[i] = ranges[i].first;
-    he[i] = ranges[i].second;
-  }
-  if (n > 1) ck(cudaMemcpyAsync(d_cols, in.cols, (size_t)(n - 1) * n * 8, cudaMemcpyHostToDevice, c.stream), "H2D cols");
-  ck(cudaMemcpyAsync(d_x0, in.x0, (size_t)n * 8, cudaMemcpyHostToDevice, c.stream), "H2D x0");
-  ck(cudaMemcpyAsync(d_s, hs.data(), nr * 8, cudaMemcpyHostToDevice, c.stream), "H2D starts");
-  ck(cudaMemcpyAsync(d_e, he.data(), nr * 8, cudaMemcpyHostToDevice, c.stream), "H2D ends");
-  const unsigned grid = (unsigned)((nr + pk::kWalkBlock - 1) / pk::kWalkBlock);
-  switch (in.policy) {
-    case PK_POLICY_DD:
-      pk::walk_dense_f64<pk::POL_DD><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, (int)nr, d_out);
-      break;
-    case PK_POLICY_KAHAN:
-      pk::walk_dense_f64<pk::POL_KAHAN><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, (int)nr, d_out);
-      break;
-    case PK_POLICY_DQ:
-      pk::walk_dense_f64<pk::POL_DQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, (int)nr, d_out);
-      break;
+int dispatch_c128(int n, const pk::C128Launch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_dense_c128<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40)
+#undef PK_CASE
     default:
-      pk::walk_dense_f64<pk::POL_QQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, (int)nr, d_out);
-      break;
+      return (int)cudaErrorInvalidValue;
   }
-  ck(cudaGetLastError(), "walk_dense_f64 launch");
 }
 
+size_t ncols_of(int n) { return (size_t)(n > 1 ? n - 1 : 1) * n; }
+
+Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact) {
+  Kind kd;
+  kd.n = n;
+  kd.streams = 1;
+  kd.logu = n >= pk::kDenseNMin ? pk::dense_logu(n) : 0;
+  const size_t nc = ncols_of(n);
+  kd.input.assign(nc + n, 0.0);
+  if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 8);
+  std::memcpy(kd.input.data() + nc, x0, (size_t)n * 8);
+  const double* h_cols = cols;
+  const double* h_x0 = x0;
+  kd.fast = [=](DevCtx& c, const double*, uint64_t chunk_lo, uint64_t groups, uint64_t g_end,
+                int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+    pk::DenseLaunch a{};
+    a.cols = h_cols;
+    a.x0 = h_x0;
+    a.policy = policy;
+    a.exact = exact;
+    a.k = k;
+    a.chunk_lo = chunk_lo;
+    a.num_groups = groups;
+    a.g_end = g_end;
+    a.group_part = gparts;
+    a.chunk_part = cparts;
+    a.out = out;
+    a.counter = c.counter;
+    a.stream = c.stream;
+    a.sms = c.sms;
+    return dispatch_dense(n, a);
+  };
+  kd.walk = [=](DevCtx& c, const double* d_in, const unsigned long long* d_s,
+                const unsigned long long* d_e, int nr, dd_t* out) {
+    const double* d_cols = d_in;
+    const double* d_x0 = d_in + nc;
+    const unsigned grid = (unsigned)((nr + pk::kWalkBlock - 1) / pk::kWalkBlock);
+    switch (policy) {
+      case PK_POLICY_DD:
+        pk::walk_dense_f64<pk::POL_DD><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, nr, out);
+        break;
+      case PK_POLICY_KAHAN:
+        pk::walk_dense_f64<pk::POL_KAHAN><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, nr, out);
+        break;
+      case PK_POLICY_DQ:
+        pk::walk_dense_f64<pk::POL_DQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, nr, out);
+        break;
+      default:
+        pk::walk_dense_f64<pk::POL_QQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, d_s, d_e, nr, out);
+        break;
+    }
+    ck(cudaGetLastError(), "walk_dense_f64 launch");
+  };
+  return kd;
+}
+
+Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact) {
+  Kind kd;
+  kd.n = n;
+  kd.streams = 2;
+  kd.logu = (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
+  const size_t nc = 2 * ncols_of(n);
+  kd.input.assign(nc + 2 * n, 0.0);
+  if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
+  std::memcpy(kd.input.data() + nc, x0, (size_t)n * 16);
+  const double* h_x0 = x0;
+  kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+    pk::C128Launch a{};
+    a.d_cols = d_in;
+    a.x0 = h_x0;
+    a.exact = exact;
+    a.k = k;
+    a.chunk_lo = chunk_lo;
+    a.num_groups = groups;
+    a.g_end = g_end;
+    a.group_part = gparts;
+    a.chunk_part = cparts;
+    a.out = out;
+    a.counter = c.counter;
+    a.stream = c.stream;
+    a.sms = c.sms;
+    return dispatch_c128(n, a);
+  };
+  kd.walk = [=](DevCtx& c, const double* d_in, const unsigned long long* d_s,
+                const unsigned long long* d_e, int nr, dd_t* out) {
+    const unsigned grid = (unsigned)((nr + pk::kWalkBlock - 1) / pk::kWalkBlock);
+    pk::walk_dense_c128<<<grid, pk::kWalkBlock, 0, c.stream>>>(d_in, d_in + nc, n, d_s, d_e, nr, out);
+    ck(cudaGetLastError(), "walk_dense_c128 launch");
+  };
+  return kd;
+}
+
+// ---------------------------------------------------------------------------
+// shared driver
+
 struct DevResult {
-  dd_t fast{0.0, 0.0};
-  std::vector<dd_t> head, tail;
+  dd_t fast[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  std::vector<dd_t> head, tail;  // walker partials
   float ms = 0.f;
   int launches = 0;
   int code = PK_OK;
   std::string err;
 };
 
-void run_dense_on_device(int dev, const DenseInputs& in, const DensePlan& pl, uint64_t g_lo,
-                         uint64_t g_cnt, bool walkers, uint64_t g_end, DevResult& r) {
+// inputs + range bounds in the device scratch area; returns d_in
+const double* upload(DevCtx& c, const Kind& kd, const std::vector<Range>& ranges,
+                     const unsigned long long** d_s, const unsigned long long** d_e) {
+  const size_t nin = kd.input.size();
+  const size_t nr = ranges.size();
+  ensure(c.scratch, c.scratch_cap, nin * 8 + nr * 16 + 64);
+  double* d_in = (double*)c.scratch;
+  unsigned long long* s = (unsigned long long*)(d_in + nin);
+  unsigned long long* e = s + nr;
+  ck(cudaMemcpyAsync(d_in, kd.input.data(), nin * 8, cudaMemcpyHostToDevice, c.stream), "H2D inputs");
+  if (nr) {
+    std::vector<unsigned long long> hb(2 * nr);
+    for (size_t i = 0; i < nr; ++i) {
+      hb[i] = ranges[i].first;
+      hb[nr + i] = ranges[i].second;
+    }
+    ck(cudaMemcpyAsync(s, hb.data(), 2 * nr * 8, cudaMemcpyHostToDevice, c.stream), "H2D ranges");
+    ck(cudaStreamSynchronize(c.stream), "H2D ranges");  // hb is stack memory
+  }
+  *d_s = s;
+  *d_e = e;
+  return d_in;
+}
+
+void run_on_device(int dev, const Kind& kd, const DensePlan& pl, uint64_t g_lo, uint64_t g_cnt,
+                   bool walkers, uint64_t g_end, DevResult& r) {
   try {
     DevCtx& c = dev_ctx(dev);
     std::lock_guard<std::mutex> lock(c.mu);
     ck(cudaSetDevice(dev), "cudaSetDevice");
-    ck(cudaEventRecord(c.e0, c.stream), "event record");
-    if (g_cnt > 0) {
-      ensure(c.groups, c.groups_cap, g_cnt);
-      pk::DenseLaunch a{};
-      a.cols = in.cols;
-      a.x0 = in.x0;
-      a.policy = in.policy;
-      a.exact = in.exact;
-      a.k = pl.k;
-      a.chunk_lo = pl.chunk_lo + 32 * g_lo;
-      a.num_groups = g_cnt;
-      a.g_end = g_end;
-      a.group_part = c.groups;
-      a.chunk_part = nullptr;
-      a.out = c.out;
-      a.counter = c.counter;
-      a.stream = c.stream;
-      a.sms = c.sms;
-      ck((cudaError_t)dispatch_dense(in.n, a), "dense_f64 register kernel launch");
-      ++r.launches;
-    }
     std::vector<Range> pieces;
     if (walkers) {
       pieces = pl.head;
       pieces.insert(pieces.end(), pl.tail.begin(), pl.tail.end());
     }
-    dd_t* d_walk = nullptr;
+    const unsigned long long *d_s, *d_e;
+    const double* d_in = upload(c, kd, pieces, &d_s, &d_e);
+    ck(cudaEventRecord(c.e0, c.stream), "event record");
+    if (g_cnt > 0) {
+      ensure(c.groups, c.groups_cap, kd.streams * g_cnt);
+      ck((cudaError_t)kd.fast(c, d_in, pl.chunk_lo + 32 * g_lo, g_cnt, g_end, pl.k, c.groups,
+                              nullptr, c.out),
+         "register kernel launch");
+      ++r.launches;
+    }
     if (!pieces.empty()) {
       ensure(c.chunks, c.chunks_cap, pieces.size());
-      d_walk = c.chunks;
-      launch_walk_dense(c, in, pieces, d_walk);
+      kd.walk(c, d_in, d_s, d_e, (int)pieces.size(), c.chunks);
       ++r.launches;
     }
     ck(cudaEventRecord(c.e1, c.stream), "event record");
     ck(cudaStreamSynchronize(c.stream), "kernel execution");
     ck(cudaEventElapsedTime(&r.ms, c.e0, c.e1), "event time");
-    if (g_cnt > 0) ck(cudaMemcpy(&r.fast, c.out, sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H total");
+    if (g_cnt > 0)
+      ck(cudaMemcpy(r.fast, c.out, kd.streams * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H total");
     if (!pieces.empty()) {
       std::vector<dd_t> w(pieces.size());
-      ck(cudaMemcpy(w.data(), d_walk, w.size() * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H walkers");
+      ck(cudaMemcpy(w.data(), c.chunks, w.size() * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H walkers");
       r.head.assign(w.begin(), w.begin() + pl.head.size());
       r.tail.assign(w.begin() + pl.head.size(), w.end());
     }
@@ -371,6 +468,122 @@ void run_dense_on_device(int dev, const DenseInputs& in, const DensePlan& pl, ui
     r.code = e.code;
     r.err = e.msg;
   }
+}
+
+std::vector<int> device_list(const int* devices, int ndev) {
+  std::vector<int> devs;
+  if (!devices || ndev <= 0) devs.push_back(0);
+  else devs.assign(devices, devices + ndev);
+  return devs;
+}
+
+// whole-range walk; out[s] = stream s partial as a double-double
+void drive(const Kind& kd, uint64_t start, uint64_t end, int log2_chunk,
+           const std::vector<int>& devs, dd_t out[2], pk_run_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  DensePlan pl = plan_dense(kd.n, kd.logu, start, end, log2_chunk, (int)devs.size());
+  const int nd = pl.num_groups ? (int)devs.size() : 1;
+  std::vector<DevResult> res(nd);
+  auto work = [&](int i) {
+    const uint64_t lo = pl.num_groups * i / nd, hi = pl.num_groups * (i + 1) / nd;
+    run_on_device(devs[i], kd, pl, lo, hi - lo, i == 0, end, res[i]);
+  };
+  if (nd == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int i = 0; i < nd; ++i) th.emplace_back(work, i);
+    for (auto& t : th) t.join();
+  }
+  for (auto& r : res)
+    if (r.code != PK_OK) fail(r.code, r.err);
+  // fixed combination order per stream: head pieces, device trees (pairwise
+  // over devices), tail pieces
+  for (int s = 0; s < kd.streams; ++s) {
+    dd_t total{0.0, 0.0};
+    bool have = false;
+    auto add = [&](dd_t v) {
+      total = have ? h_dd_add(total, v) : v;
+      have = true;
+    };
+    auto fold = [&](const std::vector<dd_t>& w) {
+      std::vector<dd_t> v;
+      for (auto& x : w) v.push_back(kd.stream_of(x, s));
+      return h_pairwise(v);
+    };
+    if (!res[0].head.empty()) add(fold(res[0].head));
+    if (pl.num_groups) {
+      std::vector<dd_t> trees;
+      for (auto& r : res) trees.push_back(r.fast[s]);
+      add(h_pairwise(trees));
+    }
+    if (!res[0].tail.empty()) add(fold(res[0].tail));
+    out[s] = total;
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    float mx = 0.f;
+    int launches = 0;
+    for (auto& r : res) {
+      if (r.ms > mx) mx = r.ms;
+      launches += r.launches;
+    }
+    stats->kernel_ms = mx;
+    stats->iterates = end - start + 1;
+    stats->chunks = pl.num_groups * 32;
+    stats->walker_ranges = pl.head.size() + pl.tail.size();
+    stats->log2_chunk = pl.k;
+    stats->devices = nd;
+    stats->launches = launches;
+    stats->wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+}
+
+// per-range walker partials on one device
+void drive_ranges(const Kind& kd, const uint64_t* starts, const uint64_t* ends, int nranges,
+                  int device, dd_t* out) {
+  std::vector<Range> rs(nranges);
+  for (int i = 0; i < nranges; ++i) {
+    check_range(kd.n, starts[i], ends[i]);
+    rs[i] = Range(starts[i], ends[i]);
+  }
+  DevCtx& c = dev_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  const unsigned long long *d_s, *d_e;
+  const double* d_in = upload(c, kd, rs, &d_s, &d_e);
+  ensure(c.chunks, c.chunks_cap, rs.size());
+  kd.walk(c, d_in, d_s, d_e, nranges, c.chunks);
+  ck(cudaStreamSynchronize(c.stream), "walker execution");
+  ck(cudaMemcpy(out, c.chunks, rs.size() * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H");
+}
+
+// register-kernel chunk partials on one device (parity diagnostics)
+void drive_chunks(const Kind& kd, int log2_chunk, uint64_t chunk_lo, uint64_t nchunks,
+                  int device, dd_t* out_chunks, dd_t* out_total) {
+  const int n = kd.n;
+  if (kd.logu <= 0) fail(PK_ERR_ARG, "no register kernel for this order");
+  const int k = log2_chunk;
+  if (k < kd.logu + 1 || k > n - 6) fail(PK_ERR_ARG, "log2_chunk out of range");
+  if (nchunks == 0 || nchunks % 32) fail(PK_ERR_ARG, "nchunks must be a positive multiple of 32");
+  const uint64_t T = total_iterates(n);
+  if (((chunk_lo + nchunks - 1) << k) + 1 > T || chunk_lo + nchunks > (1ull << (n - 1 - k)))
+    fail(PK_ERR_ARG, "chunks exceed the walk");
+  DevCtx& c = dev_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  const unsigned long long *d_s, *d_e;
+  const double* d_in = upload(c, kd, {}, &d_s, &d_e);
+  const uint64_t groups = nchunks / 32;
+  ensure(c.groups, c.groups_cap, kd.streams * groups);
+  ensure(c.chunks, c.chunks_cap, nchunks);
+  ck((cudaError_t)kd.fast(c, d_in, chunk_lo, groups, T, k, c.groups, c.chunks, c.out),
+     "register kernel launch");
+  ck(cudaStreamSynchronize(c.stream), "kernel execution");
+  ck(cudaMemcpy(out_total, c.out, kd.streams * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H total");
+  if (out_chunks)
+    ck(cudaMemcpy(out_chunks, c.chunks, nchunks * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H chunks");
 }
 
 }  // namespace
@@ -394,67 +607,15 @@ int pk_dense_f64(const double* cols, const double* x0, int n, uint64_t start, ui
                  int policy, uint32_t flags, int log2_chunk, const int* devices, int ndev,
                  double out_dd[2], pk_run_stats* stats) {
   return guarded([&] {
-    const auto t0 = std::chrono::steady_clock::now();
     check_n(n);
     check_policy(policy);
     if (!x0 || !out_dd || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
-    std::vector<int> devs;
-    if (!devices || ndev <= 0) devs.push_back(0);
-    else devs.assign(devices, devices + ndev);
-    DenseInputs in{cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0};
-    DensePlan pl = plan_dense(n, start, end, log2_chunk, (int)devs.size());
-    const int nd = pl.num_groups ? (int)devs.size() : 1;
-    std::vector<DevResult> res(nd);
-    auto work = [&](int i) {
-      const uint64_t lo = pl.num_groups * i / nd, hi = pl.num_groups * (i + 1) / nd;
-      run_dense_on_device(devs[i], in, pl, lo, hi - lo, i == 0, end, res[i]);
-    };
-    if (nd == 1) {
-      work(0);
-    } else {
-      std::vector<std::thread> th;
-      for (int i = 0; i < nd; ++i) th.emplace_back(work, i);
-      for (auto& t : th) t.join();
-    }
-    for (auto& r : res)
-      if (r.code != PK_OK) fail(r.code, r.err);
-    // fixed combination order: head pieces, device trees (pairwise over
-    // devices), tail pieces
-    std::vector<dd_t> parts;
-    dd_t total{0.0, 0.0};
-    bool have = false;
-    auto add = [&](dd_t v) {
-      total = have ? h_dd_add(total, v) : v;
-      have = true;
-    };
-    if (!res[0].head.empty()) add(h_pairwise(res[0].head));
-    if (pl.num_groups) {
-      std::vector<dd_t> trees;
-      for (auto& r : res) trees.push_back(r.fast);
-      add(h_pairwise(trees));
-    }
-    if (!res[0].tail.empty()) add(h_pairwise(res[0].tail));
-    out_dd[0] = total.hi;
-    out_dd[1] = total.lo;
-    if (stats) {
-      std::memset(stats, 0, sizeof(*stats));
-      float mx = 0.f;
-      int launches = 0;
-      for (auto& r : res) {
-        if (r.ms > mx) mx = r.ms;
-        launches += r.launches;
-      }
-      stats->kernel_ms = mx;
-      stats->iterates = end - start + 1;
-      stats->chunks = pl.num_groups * 32;
-      stats->walker_ranges = pl.head.size() + pl.tail.size();
-      stats->log2_chunk = pl.k;
-      stats->devices = nd;
-      stats->launches = launches;
-      stats->wall_ms =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    }
+    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0);
+    dd_t out[2];
+    drive(kd, start, end, log2_chunk, device_list(devices, ndev), out, stats);
+    out_dd[0] = out[0].hi;
+    out_dd[1] = out[0].lo;
   });
 }
 
@@ -467,19 +628,8 @@ int pk_dense_f64_ranges(const double* cols, const double* x0, int n, const uint6
     if (nranges < 0) fail(PK_ERR_ARG, "negative range count");
     if (nranges == 0) return;
     if (!x0 || !out_dd || !starts || !ends || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
-    std::vector<Range> rs(nranges);
-    for (int i = 0; i < nranges; ++i) {
-      check_range(n, starts[i], ends[i]);
-      rs[i] = Range(starts[i], ends[i]);
-    }
-    DevCtx& c = dev_ctx(device);
-    std::lock_guard<std::mutex> lock(c.mu);
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    ensure(c.chunks, c.chunks_cap, rs.size());
-    DenseInputs in{cols, x0, n, policy, true};
-    launch_walk_dense(c, in, rs, c.chunks);
-    ck(cudaStreamSynchronize(c.stream), "walker execution");
-    ck(cudaMemcpy(out_dd, c.chunks, rs.size() * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H");
+    Kind kd = dense_f64_kind(cols, x0, n, policy, true);
+    drive_ranges(kd, starts, ends, nranges, device, reinterpret_cast<dd_t*>(out_dd));
   });
 }
 
@@ -489,44 +639,57 @@ int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_ch
   return guarded([&] {
     check_n(n);
     check_policy(policy);
-    if (n < pk::kDenseNMin) fail(PK_ERR_ARG, "register kernels need n >= 11");
     if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
-    const int logu = pk::dense_logu(n);
-    const int k = log2_chunk;
-    if (k < logu + 1 || k > n - 6) fail(PK_ERR_ARG, "log2_chunk out of range");
-    if (nchunks == 0 || nchunks % 32) fail(PK_ERR_ARG, "nchunks must be a positive multiple of 32");
-    const uint64_t T = total_iterates(n);
-    if (((chunk_lo + nchunks - 1) << k) + 1 > T || chunk_lo + nchunks > (1ull << (n - 1 - k)))
-      fail(PK_ERR_ARG, "chunks exceed the walk");
-    DevCtx& c = dev_ctx(device);
-    std::lock_guard<std::mutex> lock(c.mu);
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    const uint64_t groups = nchunks / 32;
-    ensure(c.groups, c.groups_cap, groups);
-    ensure(c.chunks, c.chunks_cap, nchunks);
-    pk::DenseLaunch a{};
-    a.cols = cols;
-    a.x0 = x0;
-    a.policy = policy;
-    a.exact = (flags & PK_FLAG_EXACT) != 0;
-    a.k = k;
-    a.chunk_lo = chunk_lo;
-    a.num_groups = groups;
-    a.g_end = T;
-    a.group_part = c.groups;
-    a.chunk_part = c.chunks;
-    a.out = c.out;
-    a.counter = c.counter;
-    a.stream = c.stream;
-    a.sms = c.sms;
-    ck((cudaError_t)dispatch_dense(n, a), "dense_f64 register kernel launch");
-    ck(cudaStreamSynchronize(c.stream), "kernel execution");
-    dd_t tot;
-    ck(cudaMemcpy(&tot, c.out, sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H total");
-    out_total[0] = tot.hi;
-    out_total[1] = tot.lo;
-    if (out_chunks)
-      ck(cudaMemcpy(out_chunks, c.chunks, nchunks * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H chunks");
+    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0);
+    dd_t tot[2];
+    drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
+    out_total[0] = tot[0].hi;
+    out_total[1] = tot[0].lo;
+  });
+}
+
+int pk_dense_c128(const double* cols, const double* x0, int n, uint64_t start, uint64_t end,
+                  uint32_t flags, int log2_chunk, const int* devices, int ndev, double out[4],
+                  pk_run_stats* stats) {
+  return guarded([&] {
+    check_n(n);
+    if (!x0 || !out || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
+    check_range(n, start, end);
+    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0);
+    dd_t res[2];
+    drive(kd, start, end, log2_chunk, device_list(devices, ndev), res, stats);
+    out[0] = res[0].hi;
+    out[1] = res[0].lo;
+    out[2] = res[1].hi;
+    out[3] = res[1].lo;
+  });
+}
+
+int pk_dense_c128_ranges(const double* cols, const double* x0, int n, const uint64_t* starts,
+                         const uint64_t* ends, int nranges, int device, double* out) {
+  return guarded([&] {
+    check_n(n);
+    if (nranges < 0) fail(PK_ERR_ARG, "negative range count");
+    if (nranges == 0) return;
+    if (!x0 || !out || !starts || !ends || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
+    Kind kd = dense_c128_kind(cols, x0, n, true);
+    drive_ranges(kd, starts, ends, nranges, device, reinterpret_cast<dd_t*>(out));
+  });
+}
+
+int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_chunk,
+                         uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
+                         double* out_chunks, double out_total[4]) {
+  return guarded([&] {
+    check_n(n);
+    if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
+    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0);
+    dd_t tot[2];
+    drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
+    out_total[0] = tot[0].hi;
+    out_total[1] = tot[0].lo;
+    out_total[2] = tot[1].hi;
+    out_total[3] = tot[1].lo;
   });
 }
 

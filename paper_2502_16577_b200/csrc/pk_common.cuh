@@ -153,9 +153,53 @@ __device__ __forceinline__ void qq_mul_step(double& ph, double& pl, double xi) {
   pl = __dsub_rn(e, __dsub_rn(ph, p));
 }
 
+// compile-time trailing-zero count (column of local step q >= 1)
+__host__ __device__ constexpr int ctz_c(int q) {
+  int j = 0;
+  while (((q >> j) & 1) == 0) ++j;
+  return j;
+}
+
 // Changed column and direction for iterate g >= 1 (graycode.py:26-37):
 // j = ctz(g); the Gray bit j is set after the flip iff bit j+1 of g is 0.
 __device__ __forceinline__ int changed_col(uint64_t g) { return __ffsll((long long)g) - 1; }
 __device__ __forceinline__ bool flip_on(uint64_t g, int j) { return ((g >> (j + 1)) & 1ull) == 0; }
+
+// ---------------------------------------------------------------------------
+// complex, plain double (_loops.py:186-235). Values interleaved (re, im).
+// The reference multiplies as CPython/numba do: (ac - bd) + (ad + bc)i, one
+// rounding per operation; the column update promotes s to complex(s, 0).
+
+__device__ __forceinline__ void cmul_ref(double ar, double ai, double br, double bi, double& cr,
+                                         double& ci) {
+  cr = __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, bi));
+  ci = __dadd_rn(__dmul_rn(ar, bi), __dmul_rn(ai, br));
+}
+
+__device__ __forceinline__ void c_update_ref(double& xr, double& xi, double s, double cr,
+                                             double ci) {
+  double tr, ti;
+  cmul_ref(s, 0.0, cr, ci, tr, ti);
+  xr = __dadd_rn(xr, tr);
+  xi = __dadd_rn(xi, ti);
+}
+
+__device__ __forceinline__ void c_fold_ref(double& accr, double& acci, const double* x, int n,
+                                           bool odd) {
+  double pr = 1.0, pi = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double r, im;
+    cmul_ref(pr, pi, x[2 * i], x[2 * i + 1], r, im);
+    pr = r;
+    pi = im;
+  }
+  if (odd) {
+    accr = __dsub_rn(accr, pr);
+    acci = __dsub_rn(acci, pi);
+  } else {
+    accr = __dadd_rn(accr, pr);
+    acci = __dadd_rn(acci, pi);
+  }
+}
 
 }  // namespace pk

@@ -1,0 +1,56 @@
+// Host-side launcher template for the N-specialised dense complex kernel.
+#pragma once
+#include <cstring>
+
+#include "pk_dense_c128.cuh"
+#include "pk_launch.h"
+
+namespace pk {
+
+template <int N, class C>
+static int launch_c128_cfg(const C128Launch& a, const DenseC128Params<N>& p) {
+  auto kern = dense_c128_chunks<N, C>;
+  constexpr size_t smem = c128_smem_bytes<N>();
+  static int occ = -1;
+  if (occ < 0) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kC128Block, smem);
+    if (e != cudaSuccess) return (int)e;
+    occ = o > 0 ? o : 1;
+  }
+  const uint64_t blocks_needed = (a.num_groups * 32 + kC128Block - 1) / kC128Block;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if (blocks_needed < grid) grid = blocks_needed;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kC128Block, smem, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_dense_c128(const C128Launch& a) {
+  static_assert(N >= kC128NMin && N <= kC128NMax, "order out of range");
+  constexpr int LOGU = c128_logu(N);
+  constexpr int MB = c128_minb(N);
+  DenseC128Params<N> p;
+  std::memcpy(p.x0, a.x0, sizeof(double) * 2 * N);
+  p.cols = a.d_cols;
+  p.group_part = a.group_part;
+  p.chunk_part = a.chunk_part;
+  p.out = a.out;
+  p.counter = a.counter;
+  p.chunk_lo = a.chunk_lo;
+  p.num_groups = a.num_groups;
+  p.g_end = a.g_end;
+  p.k = a.k;
+  return a.exact ? launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p)
+                 : launch_c128_cfg<N, C128Cfg<LOGU, false, MB>>(a, p);
+}
+
+}  // namespace pk
+
+#define PK_INSTANTIATE_DENSE_C128(N) template int pk::launch_dense_c128<N>(const pk::C128Launch&);

@@ -40,12 +40,6 @@ struct DenseF64Params {
   int k;                          // log2 chunk size, k > LOGU
 };
 
-__host__ __device__ constexpr int ctz_c(int q) {
-  int j = 0;
-  while (((q >> j) & 1) == 0) ++j;
-  return j;
-}
-
 template <int N, int PS>
 __device__ __forceinline__ double row_product(const double (&x)[N]) {
   if constexpr (PS == 1) {

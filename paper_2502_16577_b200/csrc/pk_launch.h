@@ -39,4 +39,32 @@ struct DenseLaunch {
 template <int N>
 int launch_dense_f64(const DenseLaunch& a);
 
+// complex: register kernels for N in [kC128NMin, kC128NMax]; cols/x0 are
+// interleaved (re, im); cols must already be on the device (d_cols)
+constexpr int kC128NMin = 11;
+constexpr int kC128NMax = 40;
+// complex state is 4N registers; longer bodies make ptxas interleave more
+// product chains than the register file holds, so bodies stay short
+constexpr int c128_logu(int N) { return N <= 32 ? 2 : 1; }
+constexpr int c128_minb(int N) { return N <= 32 ? 2 : 1; }
+
+struct C128Launch {
+  const double* d_cols;  // device, (n-1)*n*2
+  const double* x0;      // host, 2n
+  bool exact;
+  int k;
+  uint64_t chunk_lo;
+  uint64_t num_groups;
+  uint64_t g_end;
+  dd_t* group_part;      // device [2*num_groups]
+  dd_t* chunk_part;      // device [num_groups*32] or null
+  dd_t* out;             // device [2]
+  unsigned int* counter;
+  cudaStream_t stream;
+  int sms;
+};
+
+template <int N>
+int launch_dense_c128(const C128Launch& a);
+
 }  // namespace pk

@@ -15,15 +15,16 @@
 
 namespace pk {
 
-// Pairwise fold of parts[lo, hi) in index order.
-__device__ inline dd_t pairwise_fold(const dd_t* parts, uint64_t lo, uint64_t hi) {
+// Pairwise fold of parts[i*S + s] for i in [lo, hi), in index order.
+__device__ inline dd_t pairwise_fold(const dd_t* parts, uint64_t lo, uint64_t hi, int S = 1,
+                                     int s = 0) {
   dd_t stack[64];
   int depth = 0;
   uint64_t idx = 0;
   for (uint64_t i = lo; i < hi; ++i, ++idx) {
     dd_t v;
-    v.hi = __ldcg(&parts[i].hi);
-    v.lo = __ldcg(&parts[i].lo);
+    v.hi = __ldcg(&parts[i * S + s].hi);
+    v.lo = __ldcg(&parts[i * S + s].lo);
     // merge once per trailing one of the running index
     uint64_t t = idx;
     while (t & 1ull) {
@@ -38,10 +39,11 @@ __device__ inline dd_t pairwise_fold(const dd_t* parts, uint64_t lo, uint64_t hi
 }
 
 // Called by every block at the end of a chunk kernel. The last block to
-// arrive folds all group partials into *out and re-arms the counter.
-template <int BLOCK>
-__device__ inline void grid_tail_reduce(const dd_t* parts, uint64_t count, dd_t* out,
-                                        unsigned int* counter) {
+// arrive folds the S interleaved streams of group partials (parts[i*S + s])
+// into out[s] and re-arms the counter.
+template <int BLOCK, int S>
+__device__ inline void grid_tail_reduce_streams(const dd_t* parts, uint64_t count, dd_t* out,
+                                                unsigned int* counter) {
   __shared__ bool is_last;
   __shared__ dd_t tree[BLOCK];
   __threadfence();
@@ -56,20 +58,33 @@ __device__ inline void grid_tail_reduce(const dd_t* parts, uint64_t count, dd_t*
   unsigned int b = 1;
   while (2ull * b <= (uint64_t)BLOCK && 2ull * b <= count) b *= 2;
   const unsigned int t = threadIdx.x;
-  if (t < b && count > 0) {
-    const uint64_t lo = count * t / b;
-    const uint64_t hi = count * (t + 1) / b;
-    tree[t] = pairwise_fold(parts, lo, hi);
-  }
-  __syncthreads();
-  for (unsigned int s = 1; s < b; s <<= 1) {
-    if (t < b && (t & (2 * s - 1)) == 0) tree[t] = dd_add(tree[t], tree[t + s]);
+  for (int s = 0; s < S; ++s) {
+    if (t < b && count > 0) {
+      const uint64_t lo = count * t / b;
+      const uint64_t hi = count * (t + 1) / b;
+      tree[t] = pairwise_fold(parts, lo, hi, S, s);
+    }
+    __syncthreads();
+    for (unsigned int w = 1; w < b; w <<= 1) {
+      if (t < b && (t & (2 * w - 1)) == 0) tree[t] = dd_add(tree[t], tree[t + w]);
+      __syncthreads();
+    }
+    if (t == 0) out[s] = count > 0 ? tree[0] : dd_t{0.0, 0.0};
     __syncthreads();
   }
-  if (t == 0) {
-    *out = count > 0 ? tree[0] : dd_t{0.0, 0.0};
-    *counter = 0u;
-  }
+  if (t == 0) *counter = 0u;
+}
+
+template <int BLOCK>
+__device__ inline void grid_tail_reduce(const dd_t* parts, uint64_t count, dd_t* out,
+                                        unsigned int* counter) {
+  grid_tail_reduce_streams<BLOCK, 1>(parts, count, out, counter);
+}
+
+template <int BLOCK>
+__device__ inline void grid_tail_reduce_pairs(const dd_t* parts, uint64_t count, dd_t* out,
+                                              unsigned int* counter) {
+  grid_tail_reduce_streams<BLOCK, 2>(parts, count, out, counter);
 }
 
 }  // namespace pk

@@ -83,41 +83,7 @@ __global__ void __launch_bounds__(kWalkBlock)
 }
 
 // ---------------------------------------------------------------------------
-// complex, plain double (_loops.py:186-235). Values interleaved (re, im).
-// The reference multiplies as CPython/numba do: (ac - bd) + (ad + bc)i, one
-// rounding per operation; the column update promotes s to complex(s, 0).
-
-__device__ __forceinline__ void cmul_ref(double ar, double ai, double br, double bi, double& cr,
-                                         double& ci) {
-  cr = __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, bi));
-  ci = __dadd_rn(__dmul_rn(ar, bi), __dmul_rn(ai, br));
-}
-
-__device__ __forceinline__ void c_update_ref(double& xr, double& xi, double s, double cr,
-                                             double ci) {
-  double tr, ti;
-  cmul_ref(s, 0.0, cr, ci, tr, ti);
-  xr = __dadd_rn(xr, tr);
-  xi = __dadd_rn(xi, ti);
-}
-
-__device__ __forceinline__ void c_fold_ref(double& accr, double& acci, const double* x, int n,
-                                           bool odd) {
-  double pr = 1.0, pi = 0.0;
-  for (int i = 0; i < n; ++i) {
-    double r, im;
-    cmul_ref(pr, pi, x[2 * i], x[2 * i + 1], r, im);
-    pr = r;
-    pi = im;
-  }
-  if (odd) {
-    accr = __dsub_rn(accr, pr);
-    acci = __dsub_rn(acci, pi);
-  } else {
-    accr = __dadd_rn(accr, pr);
-    acci = __dadd_rn(acci, pi);
-  }
-}
+// complex walkers (helpers in pk_common.cuh)
 
 // out[r] = (re, im) of the plain complex partial
 __global__ void __launch_bounds__(kWalkBlock)
