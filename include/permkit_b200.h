@@ -127,6 +127,32 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
                          uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
                          double* out_chunks, double out_total[4]);
 
+/* --------------------------------------------------------- exact integers
+ * a: row-major n*n int64 matrix (integer kind, matrix.py:53-63). The walk
+ * runs on z_i = y_i / 2 (even row sum) or y_i (odd row sum), y = 2x the
+ * reference's doubled state (kernels.py:104-110), so
+ *     y-space partial (run_range's PartialResult.value) = z-partial * 2^even_rows.
+ * out_z: z-space partial over [start, end] as a 192-bit two's complement
+ * integer (3 little-endian words). Exact whenever info->exact_terms is 1
+ * (every term below 2^127 in magnitude); otherwise only the low 128 bits are
+ * meaningful (the partial mod 2^128, enough to recover a whole-walk total
+ * under a permanent bound). PK_ERR_OVERFLOW if a row's absolute sum exceeds
+ * 2^31 (32-bit state). Register kernels for 11 <= n <= 63, walkers below. */
+typedef struct pk_int_info {
+  int32_t zbits;          /* |z| < 2^zbits: 5, 7, 15 or 31 */
+  int32_t even_rows;      /* rows with even sum: y-space scale 2^even_rows */
+  int32_t exact_terms;    /* 1 if the product of the row bounds is < 2^127 */
+  int32_t reserved;
+  double log2_term_bound; /* log2 of that product */
+} pk_int_info;
+
+int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, int log2_chunk,
+           const int* devices, int ndev, uint64_t out_z[3], pk_int_info* info,
+           pk_run_stats* stats);
+/* one exact partial per range (walkers, one device thread each): 3 words each */
+int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_t* ends,
+                  int nranges, int device, uint64_t* out_z, pk_int_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,8 @@
 #include "permkit_b200.h"
 #include "pk_launch.h"
 #include "pk_walker.cuh"
+#include "pk_int.cuh"
+#include <cmath>
 #include <functional>
 
 namespace {
@@ -586,6 +588,195 @@ void drive_chunks(const Kind& kd, int log2_chunk, uint64_t chunk_lo, uint64_t nc
     ck(cudaMemcpy(out_chunks, c.chunks, nchunks * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H chunks");
 }
 
+// ---------------------------------------------------------------------------
+// exact integers
+
+struct IntPrep {
+  int n = 0;
+  int zb = 31;
+  int even_rows = 0;
+  bool exact_terms = true;
+  double log2_bound = 0.0;
+  std::vector<int> zcols;  // (n-1)*n, z-space column steps
+  std::vector<int> z0;
+};
+
+// y = 2x state of kernels.py:104-110, rescaled per row (pk_int.cuh header)
+IntPrep prep_int(const int64_t* a, int n) {
+  IntPrep ip;
+  ip.n = n;
+  ip.zcols.assign((size_t)(n > 1 ? n - 1 : 1) * n, 0);
+  ip.z0.assign(n, 0);
+  const __int128 lim = ((__int128)1 << 31) - 1;
+  int64_t zmax_all = 0;
+  double lb = 0.0;
+  bool zero_row = false;
+  for (int i = 0; i < n; ++i) {
+    __int128 r = 0, R = 0;
+    for (int j = 0; j < n; ++j) {
+      const __int128 v = a[(size_t)i * n + j];
+      r += v;
+      R += v < 0 ? -v : v;
+    }
+    const bool even = (r % 2) == 0;
+    if (even) ++ip.even_rows;
+    const __int128 y0 = 2 * (__int128)a[(size_t)i * n + n - 1] - r;
+    const __int128 z0 = even ? y0 / 2 : y0;
+    const __int128 zmax = even ? R / 2 : R;  // |y_i| <= R_i along the whole walk
+    if (zmax > lim) fail(PK_ERR_OVERFLOW, "integer row sums exceed 2^31; exact GPU walk unavailable");
+    ip.z0[i] = (int)z0;
+    for (int j = 0; j < n - 1; ++j) {
+      const __int128 v = a[(size_t)i * n + j];
+      ip.zcols[(size_t)j * n + i] = (int)(even ? v : 2 * v);
+    }
+    if (zmax > zmax_all) zmax_all = (int64_t)zmax;
+    if (zmax == 0) zero_row = true;
+    else lb += std::log2((double)zmax);
+  }
+  ip.zb = zmax_all <= 31 ? 5 : zmax_all <= 127 ? 7 : zmax_all <= 32767 ? 15 : 31;
+  ip.log2_bound = zero_row ? -INFINITY : lb;
+  ip.exact_terms = zero_row || lb < 126.9;
+  return ip;
+}
+
+int dispatch_int(int n, const pk::IntLaunch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_int<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40) PK_CASE(41) PK_CASE(42) PK_CASE(43) PK_CASE(44) PK_CASE(45)
+    PK_CASE(46) PK_CASE(47) PK_CASE(48) PK_CASE(49) PK_CASE(50) PK_CASE(51) PK_CASE(52)
+    PK_CASE(53) PK_CASE(54) PK_CASE(55) PK_CASE(56) PK_CASE(57) PK_CASE(58) PK_CASE(59)
+    PK_CASE(60) PK_CASE(61) PK_CASE(62) PK_CASE(63)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+inline void h_i192_add(pk::i192& a, const pk::i192& b) {
+  unsigned __int128 lo = (unsigned __int128)a.w0 + b.w0;
+  a.w0 = (uint64_t)lo;
+  lo = (lo >> 64) + a.w1 + b.w1;
+  a.w1 = (uint64_t)lo;
+  a.w2 = a.w2 + b.w2 + (uint64_t)(lo >> 64);
+}
+
+struct IntDevResult {
+  pk::i192 sum{0, 0, 0};
+  float ms = 0.f;
+  int launches = 0;
+  int code = PK_OK;
+  std::string err;
+};
+
+// upload z-space inputs and range bounds; returns device pointers
+const int* upload_int(DevCtx& c, const IntPrep& ip, const std::vector<Range>& ranges,
+                      const unsigned long long** d_s, const unsigned long long** d_e,
+                      const int** d_z0) {
+  const size_t ncol = ip.zcols.size(), nz = ip.z0.size(), nr = ranges.size();
+  const size_t ints = ((ncol + nz) + 1) & ~size_t(1);  // keep the u64 arrays 8-byte aligned
+  ensure(c.scratch, c.scratch_cap, ints * 4 + nr * 16 + 64);
+  int* d_cols = (int*)c.scratch;
+  int* z0 = d_cols + ncol;
+  unsigned long long* s = (unsigned long long*)(d_cols + ints);
+  std::vector<int> hin(ints, 0);
+  std::memcpy(hin.data(), ip.zcols.data(), ncol * 4);
+  std::memcpy(hin.data() + ncol, ip.z0.data(), nz * 4);
+  std::vector<unsigned long long> hb(2 * nr);
+  for (size_t i = 0; i < nr; ++i) {
+    hb[i] = ranges[i].first;
+    hb[nr + i] = ranges[i].second;
+  }
+  ck(cudaMemcpyAsync(d_cols, hin.data(), ints * 4, cudaMemcpyHostToDevice, c.stream), "H2D int inputs");
+  if (nr) ck(cudaMemcpyAsync(s, hb.data(), 2 * nr * 8, cudaMemcpyHostToDevice, c.stream), "H2D ranges");
+  ck(cudaStreamSynchronize(c.stream), "H2D int inputs");
+  *d_s = s;
+  *d_e = s + nr;
+  *d_z0 = z0;
+  return d_cols;
+}
+
+void launch_walk_int(DevCtx& c, const IntPrep& ip, const int* d_cols, const int* d_z0,
+                     const unsigned long long* d_s, const unsigned long long* d_e, int nr,
+                     pk::i192* out) {
+  const unsigned grid = (unsigned)((nr + 127) / 128);
+  pk::walk_int<<<grid, 128, 0, c.stream>>>(d_cols, d_z0, ip.n, d_s, d_e, nr, out);
+  ck(cudaGetLastError(), "walk_int launch");
+}
+
+void run_int_on_device(int dev, const IntPrep& ip, const DensePlan& pl, uint64_t g_lo,
+                       uint64_t g_cnt, bool walkers, uint64_t g_end, IntDevResult& r) {
+  try {
+    DevCtx& c = dev_ctx(dev);
+    std::lock_guard<std::mutex> lock(c.mu);
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    std::vector<Range> pieces;
+    if (walkers) {
+      pieces = pl.head;
+      pieces.insert(pieces.end(), pl.tail.begin(), pl.tail.end());
+    }
+    const unsigned long long *d_s, *d_e;
+    const int* d_z0;
+    const int* d_cols = upload_int(c, ip, pieces, &d_s, &d_e, &d_z0);
+    ck(cudaEventRecord(c.e0, c.stream), "event record");
+    // i192 buffers are carved from the dd workspaces (24 B <= 32 B per dd pair)
+    if (g_cnt > 0) {
+      ensure(c.groups, c.groups_cap, g_cnt);
+      pk::IntLaunch a{};
+      a.d_cols = d_cols;
+      a.z0 = ip.z0.data();
+      a.zb = ip.zb;
+      a.k = pl.k;
+      a.chunk_lo = pl.chunk_lo + 32 * g_lo;
+      a.num_groups = g_cnt;
+      a.g_end = g_end;
+      a.group_part = c.groups;
+      a.chunk_part = nullptr;
+      a.out = c.out;
+      a.counter = c.counter;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      ck((cudaError_t)dispatch_int(ip.n, a), "int register kernel launch");
+      ++r.launches;
+    }
+    if (!pieces.empty()) {
+      ensure(c.chunks, c.chunks_cap, pieces.size());
+      launch_walk_int(c, ip, d_cols, d_z0, d_s, d_e, (int)pieces.size(), (pk::i192*)c.chunks);
+      ++r.launches;
+    }
+    ck(cudaEventRecord(c.e1, c.stream), "event record");
+    ck(cudaStreamSynchronize(c.stream), "kernel execution");
+    ck(cudaEventElapsedTime(&r.ms, c.e0, c.e1), "event time");
+    if (g_cnt > 0) {
+      pk::i192 t;
+      ck(cudaMemcpy(&t, c.out, sizeof(t), cudaMemcpyDeviceToHost), "D2H total");
+      h_i192_add(r.sum, t);
+    }
+    if (!pieces.empty()) {
+      std::vector<pk::i192> w(pieces.size());
+      ck(cudaMemcpy(w.data(), c.chunks, w.size() * sizeof(pk::i192), cudaMemcpyDeviceToHost), "D2H walkers");
+      for (auto& v : w) h_i192_add(r.sum, v);
+    }
+  } catch (const PkError& e) {
+    r.code = e.code;
+    r.err = e.msg;
+  }
+}
+
+void fill_info(const IntPrep& ip, pk_int_info* info) {
+  if (!info) return;
+  info->zbits = ip.zb;
+  info->even_rows = ip.even_rows;
+  info->exact_terms = ip.exact_terms ? 1 : 0;
+  info->reserved = 0;
+  info->log2_term_bound = ip.log2_bound;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -690,6 +881,88 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
     out_total[1] = tot[0].lo;
     out_total[2] = tot[1].hi;
     out_total[3] = tot[1].lo;
+  });
+}
+
+int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, int log2_chunk,
+           const int* devices, int ndev, uint64_t out_z[3], pk_int_info* info,
+           pk_run_stats* stats) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_n(n);
+    if (!a || !out_z) fail(PK_ERR_ARG, "null pointer argument");
+    check_range(n, start, end);
+    IntPrep ip = prep_int(a, n);
+    fill_info(ip, info);
+    std::vector<int> devs = device_list(devices, ndev);
+    const int logu = n >= pk::kIntNMin ? pk::int_logu(n) : 0;
+    DensePlan pl = plan_dense(n, logu, start, end, log2_chunk, (int)devs.size());
+    const int nd = pl.num_groups ? (int)devs.size() : 1;
+    std::vector<IntDevResult> res(nd);
+    auto work = [&](int i) {
+      const uint64_t lo = pl.num_groups * i / nd, hi = pl.num_groups * (i + 1) / nd;
+      run_int_on_device(devs[i], ip, pl, lo, hi - lo, i == 0, end, res[i]);
+    };
+    if (nd == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int i = 0; i < nd; ++i) th.emplace_back(work, i);
+      for (auto& t : th) t.join();
+    }
+    pk::i192 total{0, 0, 0};
+    for (auto& r : res) {
+      if (r.code != PK_OK) fail(r.code, r.err);
+      h_i192_add(total, r.sum);
+    }
+    out_z[0] = total.w0;
+    out_z[1] = total.w1;
+    out_z[2] = total.w2;
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      float mx = 0.f;
+      int launches = 0;
+      for (auto& r : res) {
+        if (r.ms > mx) mx = r.ms;
+        launches += r.launches;
+      }
+      stats->kernel_ms = mx;
+      stats->iterates = end - start + 1;
+      stats->chunks = pl.num_groups * 32;
+      stats->walker_ranges = pl.head.size() + pl.tail.size();
+      stats->log2_chunk = pl.k;
+      stats->devices = nd;
+      stats->launches = launches;
+      stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_t* ends,
+                  int nranges, int device, uint64_t* out_z, pk_int_info* info) {
+  return guarded([&] {
+    check_n(n);
+    if (nranges < 0) fail(PK_ERR_ARG, "negative range count");
+    if (!a || (nranges > 0 && (!out_z || !starts || !ends))) fail(PK_ERR_ARG, "null pointer argument");
+    IntPrep ip = prep_int(a, n);
+    fill_info(ip, info);
+    if (nranges == 0) return;
+    std::vector<Range> rs(nranges);
+    for (int i = 0; i < nranges; ++i) {
+      check_range(n, starts[i], ends[i]);
+      rs[i] = Range(starts[i], ends[i]);
+    }
+    DevCtx& c = dev_ctx(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const unsigned long long *d_s, *d_e;
+    const int* d_z0;
+    const int* d_cols = upload_int(c, ip, rs, &d_s, &d_e, &d_z0);
+    ensure(c.chunks, c.chunks_cap, rs.size());
+    launch_walk_int(c, ip, d_cols, d_z0, d_s, d_e, nranges, (pk::i192*)c.chunks);
+    ck(cudaStreamSynchronize(c.stream), "walker execution");
+    ck(cudaMemcpy(out_z, c.chunks, rs.size() * sizeof(pk::i192), cudaMemcpyDeviceToHost), "D2H");
   });
 }
 

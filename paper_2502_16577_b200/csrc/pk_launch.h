@@ -67,4 +67,29 @@ struct C128Launch {
 template <int N>
 int launch_dense_c128(const C128Launch& a);
 
+// exact integers (pk_int.cuh): z-space state, |z_i| < 2^zb
+constexpr int kIntNMin = 11;
+constexpr int kIntNMax = 63;
+constexpr int int_logu(int N) { return 2; }
+constexpr int int_minb(int N) { return N <= 40 ? 4 : (N <= 52 ? 3 : 2); }
+
+struct IntLaunch {
+  const int* d_cols;     // device, z-space column steps, (n-1)*n
+  const int* z0;         // host, n
+  int zb;                // 5, 7, 15 or 31
+  int k;
+  uint64_t chunk_lo;
+  uint64_t num_groups;
+  uint64_t g_end;
+  void* group_part;      // device i192 [num_groups]
+  void* chunk_part;      // device i192 [num_groups*32] or null
+  void* out;             // device i192 [1]
+  unsigned int* counter;
+  cudaStream_t stream;
+  int sms;
+};
+
+template <int N>
+int launch_int(const IntLaunch& a);
+
 }  // namespace pk

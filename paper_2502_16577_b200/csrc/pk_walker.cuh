@@ -10,6 +10,7 @@
 // that is acceptable here because walkers never carry the bulk of a walk.
 #pragma once
 #include "pk_common.cuh"
+#include "pk_int.cuh"
 
 namespace pk {
 
@@ -144,6 +145,38 @@ __global__ void __launch_bounds__(kWalkBlock)
     if (g == end) break;
   }
   out[r] = dd_t{accr, acci};
+}
+
+// ---------------------------------------------------------------------------
+// range walker: run-time n, exact product by repeated 128-bit wrapping
+// multiply (exact under the same host bound), one thread per range
+
+__global__ void __launch_bounds__(128)
+    walk_int(const int* __restrict__ cols, const int* __restrict__ z0, int n,
+             const unsigned long long* __restrict__ starts,
+             const unsigned long long* __restrict__ ends, int nranges, i192* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nranges) return;
+  const uint64_t start = starts[r], end = ends[r];
+  int z[64];
+  for (int i = 0; i < n; ++i) z[i] = z0[i];
+  uint64_t code = (start - 1) ^ ((start - 1) >> 1);
+  for (int j = 0; code; ++j, code >>= 1)
+    if (code & 1ull)
+      for (int i = 0; i < n; ++i) z[i] += cols[j * n + i];
+  i192 acc{0ull, 0ull, 0ull};
+  for (uint64_t g = start;; ++g) {
+    const int j = changed_col(g);
+    const int s = flip_on(g, j) ? 1 : -1;
+    const int* c = cols + (size_t)j * n;
+    for (int i = 0; i < n; ++i) z[i] += s * c[i];
+    unsigned __int128 p = 1;
+    for (int i = 0; i < n; ++i) p *= (unsigned __int128)(__int128)z[i];
+    const unsigned long long lo = (unsigned long long)p, hi = (unsigned long long)(p >> 64);
+    if (g & 1ull) i192_sub128(acc, lo, hi); else i192_add128(acc, lo, hi);
+    if (g == end) break;
+  }
+  out[r] = acc;
 }
 
 }  // namespace pk
