@@ -43,7 +43,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=40)
+    ap.add_argument("--workload", default="dense", choices=["dense", "binary", "haar"],
+                    help="dense: n x n random [0,1) real (the metric's workload); binary: "
+                         "n x n 0/1 density 0.3, exact (config 3); haar: n x n block of a "
+                         "Haar unitary, complex (config 4)")
+    ap.add_argument("--n", type=int, default=0, help="order (default 40 / 40 / 32)")
     ap.add_argument("--policy", default="kahan")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -235,6 +239,7 @@ def matrix_rows(n):
 def run_reference(args, dist: Dist):
     if dist.rank != 0:
         return 0
+    args.n = args.n or 40
     rows = matrix_rows(args.n)
     samples = []
     log2 = min(args.cpu_sample_log2 - 2, args.n - 2)
@@ -262,78 +267,150 @@ def run_reference(args, dist: Dist):
     return 0
 
 
+class Workload:
+    """One bench configuration: matrix, per-rank walk, exact host combine."""
+
+    def __init__(self, args):
+        import paper_2502_16577_b200 as pk
+        self.kind = args.workload
+        self.n = args.n or (32 if self.kind == "haar" else 40)
+        n = self.n
+        self.policy = args.policy if self.kind == "dense" else "dd"
+        if self.kind == "dense":
+            self.rows = matrix_rows(n)
+            self.m = pk.DenseMatrix.from_rows(self.rows)
+            self.flops = 3 * n
+            self.desc = (f"n={n} dense real fp64 permanent, random [0,1) seed {SEED}, policy "
+                         f"{self.policy}, whole Gray walk (2^{n - 1}-1 updates) per step")
+        elif self.kind == "binary":
+            d = pk.random_binary(n, SEED, 0.3)
+            self.rows = d.rows()
+            self.m = pk.dense_to_sparse(d)
+            self.flops = None
+            self.desc = (f"n={n} sparse 0/1 matrix density 0.3 seed {SEED} (SpaRyser, exact "
+                         f"int), whole walk per step")
+        else:
+            self.m = pk.haar_unitary_block(n, SEED)
+            self.rows = self.m.rows()
+            self.flops = 10 * n
+            self.desc = (f"n={n} complex fp64 top-left block of a Haar U({n * n}) seed {SEED}, "
+                         f"whole walk per step")
+
+    def walk(self, lo, hi, devices):
+        """(partial as a list of floats for the gather, stats)"""
+        from paper_2502_16577_b200 import _native
+        from paper_2502_16577_b200.precision import AccumulatorPolicy
+        st = _native.RunStats()
+        if self.kind == "dense":
+            from paper_2502_16577_b200.kernels import DenseF64Problem
+            p = DenseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
+                                            devices=devices, stats=st)
+            return [p.hi, p.lo], st
+        if self.kind == "haar":
+            from paper_2502_16577_b200.complex_walk import DenseC128Problem
+            r, i = DenseC128Problem(self.m).walk(lo, hi, devices=devices, stats=st)
+            return [r.hi, r.lo, i.hi, i.lo], st
+        from paper_2502_16577_b200.integer import IntProblem
+        words, info = IntProblem(self.m).walk(lo, hi, devices=devices, stats=st)
+        self.even_rows = info.even_rows
+        # 192-bit words travel as exact float64 pieces of 32 bits
+        return [float((w >> (32 * h)) & 0xFFFFFFFF) for w in words for h in (0, 1)], st
+
+    def combine(self, gathered):
+        """fixed rank-order host reduction + the g = 0 term -> permanent"""
+        from paper_2502_16577_b200.kernels import (DenseF64Problem, _sign_factor,
+                                                   policy_product)
+        from paper_2502_16577_b200.precision import (AccumulatorPolicy, DoubleDouble, dd_add,
+                                                     dd_pairwise)
+        n = self.n
+        if self.kind == "dense":
+            p0 = policy_product(DenseF64Problem(self.m).x0, AccumulatorPolicy.parse(self.policy))
+            acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+            acc = dd_add(acc, dd_pairwise([tuple(g[:2]) for g in gathered]))
+            return (acc.hi * _sign_factor(n)).hex()
+        if self.kind == "haar":
+            from paper_2502_16577_b200.complex_walk import DenseC128Problem
+            p0 = DenseC128Problem(self.m).p0()
+            re = dd_add(DoubleDouble(p0.real, 0.0), dd_pairwise([tuple(g[0:2]) for g in gathered]))
+            im = dd_add(DoubleDouble(p0.imag, 0.0), dd_pairwise([tuple(g[2:4]) for g in gathered]))
+            s = _sign_factor(n)
+            return [(re.hi * s).hex(), (im.hi * s).hex()]
+        from paper_2502_16577_b200.integer import IntProblem, _signed, finalize_int
+        total = 0
+        for g in gathered:
+            ws = [int(g[2 * i]) | (int(g[2 * i + 1]) << 32) for i in range(3)]
+            total += _signed(ws, 192)
+        y = (total << self.even_rows) + IntProblem(self.m).p0_y()
+        return str(finalize_int(y, n))
+
+    def public_call(self):
+        import paper_2502_16577_b200 as pk
+        return pk.permanent(self.m if self.kind != "dense" else self.rows, self.policy)
+
+    def input_bytes(self):
+        n = self.n
+        if self.kind == "dense":
+            return 2 * ((n - 1) * n * 8 + n * 8)  # kernel parameter block + workspace copy
+        if self.kind == "haar":
+            return (n - 1) * n * 16 + 2 * n * 16
+        return (n - 1) * n * 4 + n * 4
+
+
 def run_b200(args, dist: Dist):
     sys.path.insert(0, ROOT)
-    import paper_2502_16577_b200 as pk
     from paper_2502_16577_b200 import _native
-    from paper_2502_16577_b200.kernels import DenseF64Problem, policy_product, _sign_factor
-    from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_add, dd_pairwise
 
-    n, N, rank = args.n, dist.world, dist.rank
-    pol = AccumulatorPolicy.parse(args.policy)
-    rows = matrix_rows(n)
-    m = pk.DenseMatrix.from_rows(rows)
+    wl = Workload(args)
+    n, N, rank = wl.n, dist.world, dist.rank
     total = (1 << (n - 1)) - 1
     span = (1 << (n - 1)) // N
     lo, hi = rank * span + 1, min((rank + 1) * span, total)
     dev = [dist.local]
     flusher = L2Flusher(dist.local)
 
-    def step_device():
-        st = _native.RunStats()
-        prob = DenseF64Problem(m)  # host marshalling is part of every call
-        part = prob.walk(lo, hi, pol, devices=dev, stats=st)
-        return part, st
-
     def step_e2e():
-        # the public API path, host matrix in, host scalar out
         t0 = time.perf_counter()
         if N == 1:
-            v = pk.permanent(rows, args.policy)
+            wl.public_call()
         else:
-            part, _ = step_device()
-            v = part
-        return v, (time.perf_counter() - t0) * 1e3
+            wl.walk(lo, hi, dev)
+        return (time.perf_counter() - t0) * 1e3
 
     for _ in range(args.warmup):
-        step_device()
+        wl.walk(lo, hi, dev)
         step_e2e()
     sync_device()
 
     peak_tf = _native.fp64_peak_tflops(dist.local)
     clocks = ClockSampler(dist.local)
     clocks.start()
-    kernel_ms, wall_ms, launches, parts = [], [], 0, []
+    kernel_ms, wall_ms, launches = [], [], 0
     for _ in range(args.steps):
         flusher.flush()
         dist.barrier()
         sync_device()
         t0 = time.perf_counter()
-        part, st = step_device()
+        part, st = wl.walk(lo, hi, dev)
         sync_device()
-        w = (time.perf_counter() - t0) * 1e3
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
         dist.barrier()
         kernel_ms.append(st.kernel_ms)
-        wall_ms.append(w)
         launches += st.launches
-        parts.append(part)
         k_used = st.log2_chunk
     e2e_ms = []
     for _ in range(args.steps):
         flusher.flush()
         dist.barrier()
         sync_device()
-        _, w = step_e2e()
+        e2e_ms.append(step_e2e())
         sync_device()
         dist.barrier()
-        e2e_ms.append(w)
     clocks.stop()
 
-    # max over ranks, per step
     g_k = dist.gather_f64(kernel_ms)
     g_w = dist.gather_f64(wall_ms)
     g_e = dist.gather_f64(e2e_ms)
-    g_part = dist.gather_f64([parts[-1].hi, parts[-1].lo])
+    g_part = dist.gather_f64(part)
     g_launch = dist.gather_f64([float(launches)])
     if rank != 0:
         return 0
@@ -342,26 +419,29 @@ def run_b200(args, dist: Dist):
     step_e = [max(g[i] for g in g_e) for i in range(args.steps)]
     ups = args.steps * total / (sum(step_k) * 1e-3)
     e2e_ups = args.steps * total / (sum(step_e) * 1e-3)
+    result = wl.combine(g_part)
 
-    # fixed-order host reduction of the per-GPU partials (+ the g = 0 term)
-    x0 = DenseF64Problem(m).x0
-    p0 = policy_product(x0, pol)
-    acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
-    acc = dd_add(acc, dd_pairwise([tuple(g) for g in g_part]))
-    perm = acc.hi * _sign_factor(n)
-
-    flops_per_update = 3 * n
-    # per launch: one walk kernel per GPU per step, timed with CUDA events
-    achieved_tf = flops_per_update * (total / N) / (statistics.mean(step_k) * 1e-3) * 1e-12
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
+    if wl.flops:
+        achieved_tf = wl.flops * (total / N) / (statistics.mean(step_k) * 1e-3) * 1e-12
+        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": achieved_tf / peak_tf, "traffic": None,
+                    "note": f"algorithmic {wl.flops} flop/update x updates per launch / CUDA-event "
+                            "time of that launch; peak = live DFMA microbenchmark (pk_fp64_peak); "
+                            "MEASURED_PEAKS.json has no FP64 entry (hbm_gbs=%s, bf16_tflops=%s); "
+                            "HBM traffic is ~0 (inputs < 32 KB)" % (peaks.get("hbm_gbs"),
+                                                                    peaks.get("bf16_tflops"))}
+    else:
+        roofline = {"bound": "int-issue", "achieved": None, "peak": None, "unit": "updates/s",
+                    "frac": None, "traffic": None,
+                    "note": "exact integer walk: IMAD/IADD issue bound, no FP64 roofline"}
     cpu = None
-    if not args.no_cpu_baseline and N == 1:
-        cpu = cpu_updates_per_s(n, args.policy, args.cpu_sample_log2, rows)
-    input_bytes = (n - 1) * n * 8 + n * 8
+    if not args.no_cpu_baseline and N == 1 and wl.kind == "dense":
+        cpu = cpu_updates_per_s(n, wl.policy, args.cpu_sample_log2, wl.rows)
     line = {
         "metric": METRIC,
         "value": ups,
@@ -373,29 +453,22 @@ def run_b200(args, dist: Dist):
         "wall_ms_per_step": statistics.mean(step_w),
         "higher_is_better": True,
         "scaling": "strong",
-        "vs_baseline": ups / PAPER_N40_UPS if n == 40 else None,
+        "vs_baseline": ups / PAPER_N40_UPS if (n == 40 and wl.kind == "dense") else None,
         "vs_baseline_ref": "SUperman best kernel on a Quadro GV100, n=40 in 14.17 s "
                            "(PAPER.md:785) = 3.88e10 updates/s",
-        "dtype": "f64",
+        "dtype": {"dense": "f64", "haar": "c128 (f64 pairs)", "binary": "int32 state, exact "
+                  "int128 products, 192-bit sums"}[wl.kind],
         "data": "synthetic",
-        "config": {"workload": f"n={n} dense real fp64 permanent, random [0,1) seed {SEED}, "
-                               f"policy {args.policy}, whole Gray walk (2^{n - 1}-1 updates) "
-                               f"per step", "n": n, "policy": args.policy,
+        "config": {"workload": wl.desc, "n": n, "policy": wl.policy,
                    "split": f"{N} contiguous power-of-two iterate ranges, one per GPU",
                    "log2_chunk": k_used, "l2": "flushed (256 MiB write) between steps",
-                   "permanent": perm.hex()},
-        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf,
-                     "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
-                     "traffic": None,
-                     "note": f"algorithmic {flops_per_update} flop/update (n DFMA-equivalent adds, "
-                             "n-1 DMUL, 1 accumulate) x updates per launch / event time; peak = "
-                             "live DFMA microbenchmark (pk_fp64_peak; MEASURED_PEAKS.json has no "
-                             "FP64 entry, hbm_gbs=%s bf16=%s)" % (peaks.get("hbm_gbs"),
-                                                                  peaks.get("bf16_tflops"))},
+                   "permanent": result},
+        "roofline": roofline,
         "e2e": {"value": e2e_ups, "unit": "updates/s",
-                "h2d_bytes_per_step": 2 * input_bytes * N, "d2h_bytes_per_step": 16 * N,
+                "h2d_bytes_per_step": wl.input_bytes() * N, "d2h_bytes_per_step": 48 * N,
                 "ms_per_step": statistics.mean(step_e),
-                "path": "paper_2502_16577_b200.permanent(rows) (N=1) / walk(range) per rank"},
+                "path": "paper_2502_16577_b200.permanent(host matrix) at N=1; per-rank range "
+                        "walk through the C ABI at N>1"},
         "gpu_launches": int(sum(g[0] for g in g_launch)),
         "clocks": clocks.summary(),
     }

@@ -136,7 +136,7 @@ def test_device_split_reproduces_single_device_bits():
         assert one == two == four
 
 
-@pytest.mark.parametrize("n", [14, 22, 27])
+@pytest.mark.parametrize("n", [14, 22, 25])
 def test_unaligned_ranges_fast_path(n):
     # head / middle / tail split of an arbitrary range vs the exact walker
     a = np.random.default_rng(n).uniform(-1.0, 1.0, size=(n, n))
@@ -149,7 +149,7 @@ def test_unaligned_ranges_fast_path(n):
         e = int(rng.integers(2 * T // 3, T + 1))
         st = pk._native.RunStats()
         fast = prob.walk(s, e, AccumulatorPolicy.KAHAN, stats=st)
-        ref = oracle.dense_f64_range(a, s, e, "qq")
+        ref = oracle.dense_f64_range(a, s, e, "dq")
         scale = float(np.prod(np.abs(a).sum(axis=1)))  # bound on |terms|
         assert abs((fast.hi + fast.lo) - (ref[0] + ref[1])) <= 1e-12 * scale
         assert st.iterates == e - s + 1
