@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--policy", default="kahan")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--range-log2", type=int, default=0,
+                    help="profiling aid: walk only iterates [1, 2^x] (same kernels)")
     ap.add_argument("--cpu-sample-log2", type=int, default=31,
                     help="iterates of the n-walk timed for the CPU baseline (2^x)")
     return ap.parse_args()
@@ -363,14 +365,16 @@ def run_b200(args, dist: Dist):
     wl = Workload(args)
     n, N, rank = wl.n, dist.world, dist.rank
     total = (1 << (n - 1)) - 1
-    span = (1 << (n - 1)) // N
+    if args.range_log2:
+        total = min(total, 1 << args.range_log2)
+    span = (1 << (n - 1)) // N if not args.range_log2 else max(1, total // N)
     lo, hi = rank * span + 1, min((rank + 1) * span, total)
     dev = [dist.local]
     flusher = L2Flusher(dist.local)
 
     def step_e2e():
         t0 = time.perf_counter()
-        if N == 1:
+        if N == 1 and not args.range_log2:
             wl.public_call()
         else:
             wl.walk(lo, hi, dev)
@@ -419,7 +423,7 @@ def run_b200(args, dist: Dist):
     step_e = [max(g[i] for g in g_e) for i in range(args.steps)]
     ups = args.steps * total / (sum(step_k) * 1e-3)
     e2e_ups = args.steps * total / (sum(step_e) * 1e-3)
-    result = wl.combine(g_part)
+    result = wl.combine(g_part) if not args.range_log2 else "partial walk (profiling)"
 
     peaks = {}
     try:
