@@ -367,8 +367,11 @@ def run_b200(args, dist: Dist):
     total = (1 << (n - 1)) - 1
     if args.range_log2:
         total = min(total, 1 << args.range_log2)
-    span = (1 << (n - 1)) // N if not args.range_log2 else max(1, total // N)
-    lo, hi = rank * span + 1, min((rank + 1) * span, total)
+        span = max(1, total // N)
+        lo, hi = rank * span + 1, min((rank + 1) * span, total)
+    else:
+        from paper_2502_16577_b200.distributed import rank_span
+        lo, hi = rank_span(n, rank, N)
     dev = [dist.local]
     flusher = L2Flusher(dist.local)
 
