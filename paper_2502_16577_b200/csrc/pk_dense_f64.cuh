@@ -71,10 +71,17 @@ __device__ __forceinline__ double row_product(const double (&x)[N]) {
 //        fold the body sum once (1 policy fold per U terms instead of per
 //        term). Not bit-identical to the reference's per-term fold.
 //   MINB minimum resident blocks per SM requested from ptxas (register cap)
-template <int POL_, int PS_, int LOGU_, int CS_, bool BA_, int MINB_ = 1>
+//   BLOCK threads per block (small blocks pack more warps per SM when the
+//        register count is not a divisor-friendly number)
+//   FA   fused accumulate (with BA): the last product multiply and the body
+//        sum become one DFMA, bsum = fma(+-p', x[n-1], bsum)
+template <int POL_, int PS_, int LOGU_, int CS_, bool BA_, int MINB_ = 1, int BLOCK_ = 128,
+          bool FA_ = false>
 struct DenseCfg {
   static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, CS = CS_, MINB = MINB_;
+  static constexpr int BLOCK = BLOCK_;
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
+  static constexpr bool FA = FA_ && BA;
 };
 
 // Column-operand sources. Static steps index the columns with compile-time
@@ -153,6 +160,14 @@ struct DenseWalk {
 #pragma unroll
       for (int i = 0; i < N; ++i) qq_mul_step(ph, pl, x[i]);
       if (odd) acc.sub2(ph, pl); else acc.add2(ph, pl);
+    } else if constexpr (C::FA) {
+      // product of rows 0..N-2, then one DFMA folds the last row and the sum
+      double pr = x[0];
+#pragma unroll
+      for (int i = 1; i < N - 1; ++i) pr = __dmul_rn(pr, x[i]);
+      const double sp = odd ? -pr : pr;
+      if (first_in_body) bsum = __dmul_rn(sp, x[N - 1]);
+      else bsum = __fma_rn(sp, x[N - 1], bsum);
     } else {
       const double pr = row_product<N, C::PS>(x);
       if constexpr (C::BA) {
@@ -234,7 +249,7 @@ __device__ __forceinline__ dd_t walk_chunk(const DenseF64Params<N>& p, const dou
 }
 
 template <int N, class C>
-__global__ void __launch_bounds__(kDenseBlock, C::MINB)
+__global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_f64_chunks(const __grid_constant__ DenseF64Params<N> p) {
   extern __shared__ __align__(16) double scols[];
   if constexpr (C::CS == CS_SMEM) {
@@ -255,7 +270,7 @@ __global__ void __launch_bounds__(kDenseBlock, C::MINB)
     part = warp_tree_dd(part);
     if (lane == 0) p.group_part[grp] = part;
   }
-  grid_tail_reduce<kDenseBlock>(p.group_part, p.num_groups, p.out, p.counter);
+  grid_tail_reduce<C::BLOCK>(p.group_part, p.num_groups, p.out, p.counter);
 }
 
 template <int N, class C>

@@ -20,16 +20,16 @@ static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
       if (e != cudaSuccess) return (int)e;
     }
     int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kDenseBlock, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
     if (e != cudaSuccess) return (int)e;
     occ = o > 0 ? o : 1;
   }
   const uint64_t warps_needed = a.num_groups;
-  const uint64_t blocks_needed = (warps_needed * 32 + kDenseBlock - 1) / kDenseBlock;
+  const uint64_t blocks_needed = (warps_needed * 32 + C::BLOCK - 1) / C::BLOCK;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kDenseBlock, smem, a.stream>>>(p);
+  kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);
   return (int)cudaGetLastError();
 }
 
@@ -52,13 +52,13 @@ int launch_dense_f64(const DenseLaunch& a) {
   switch (a.policy) {
     case POL_DD:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
     case POL_KAHAN:
       return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
     case POL_DQ:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, true, MB>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
     case POL_QQ:
       return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, CS_SMEM, false, MB>>(a, p);
     default:

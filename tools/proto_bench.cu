@@ -60,7 +60,7 @@ void run_variant(const char* name, Host<N>& h, int k, unsigned long long groups_
   CK(cudaFuncGetAttributes(&fa, kern));
   int dev = 0, sms = 0, occ = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDenseBlock, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::BLOCK, smem));
   const int n = N;
   const unsigned long long total = (1ull << (n - 1)) - 1;
   unsigned long long chunks = 1ull << (n - 1 - k);
@@ -77,13 +77,13 @@ void run_variant(const char* name, Host<N>& h, int k, unsigned long long groups_
   const int grid = sms * occ;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
-  kern<<<grid, kDenseBlock, smem>>>(p);  // warm
+  kern<<<grid, C::BLOCK, smem>>>(p);  // warm
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < reps; ++r) {
     CK(cudaEventRecord(e0));
-    kern<<<grid, kDenseBlock, smem>>>(p);
+    kern<<<grid, C::BLOCK, smem>>>(p);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -125,28 +125,26 @@ int main(int argc, char** argv) {
   static Host<20> h20;
   static Host<24> h24;
   struct V { const char* name; void (*fn)(); };
-#define VAR(NM, NN, POLX, PSX, UX, CSX, BAX, MB, KK, GL, R) \
-  V{NM, [] { run_variant<NN, DenseCfg<POLX, PSX, UX, CSX, BAX, MB>>(NM, h##NN, KK, GL, R); }}
+#define VAR(NM, NN, UX, MB, BL, FA, KK, GL, R) \
+  V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, CS_SMEM, true, MB, BL, FA>>(NM, h##NN, KK, GL, R); }}
   std::vector<V> vs = {
-    VAR("40_u4_mb2", 40, POL_KAHAN, 1, 4, CS_SMEM, true, 2, 18, 23680, 2),
-    VAR("40_u4_mb3", 40, POL_KAHAN, 1, 4, CS_SMEM, true, 3, 18, 23680, 2),
-    VAR("40_u4_mb4", 40, POL_KAHAN, 1, 4, CS_SMEM, true, 4, 18, 23680, 2),
-    VAR("40_u3_mb3", 40, POL_KAHAN, 1, 3, CS_SMEM, true, 3, 18, 23680, 2),
-    VAR("40_u4_ps2_mb3", 40, POL_KAHAN, 2, 4, CS_SMEM, true, 3, 18, 23680, 2),
-    VAR("40_u5_mb2", 40, POL_KAHAN, 1, 5, CS_SMEM, true, 2, 18, 23680, 2),
-    VAR("48_u3_mb2", 48, POL_KAHAN, 1, 3, CS_SMEM, true, 2, 20, 4736, 2),
-    VAR("48_u3_mb3", 48, POL_KAHAN, 1, 3, CS_SMEM, true, 3, 20, 4736, 2),
-    VAR("48_u4_mb3", 48, POL_KAHAN, 1, 4, CS_SMEM, true, 3, 20, 4736, 2),
-    VAR("48_u4_mb2", 48, POL_KAHAN, 1, 4, CS_SMEM, true, 2, 20, 4736, 2),
-    VAR("36_u4_mb2", 36, POL_KAHAN, 1, 4, CS_SMEM, true, 2, 14, 0, 3),
-    VAR("36_u4_mb3", 36, POL_KAHAN, 1, 4, CS_SMEM, true, 3, 14, 0, 3),
-    VAR("36_u4_mb4", 36, POL_KAHAN, 1, 4, CS_SMEM, true, 4, 14, 0, 3),
-    VAR("56_u3_mb2", 56, POL_KAHAN, 1, 3, CS_SMEM, true, 2, 20, 4736, 1),
-    VAR("56_u3_mb3", 56, POL_KAHAN, 1, 3, CS_SMEM, true, 3, 20, 4736, 1),
-    VAR("63_u3_mb2", 63, POL_KAHAN, 1, 3, CS_SMEM, true, 2, 20, 4736, 1),
-    VAR("63_u2_mb2", 63, POL_KAHAN, 1, 2, CS_SMEM, true, 2, 20, 4736, 1),
-    VAR("20_u4_mb2", 20, POL_KAHAN, 1, 4, CS_SMEM, true, 2, 5, 0, 5),
-    VAR("24_u4_mb3", 24, POL_KAHAN, 1, 4, CS_SMEM, true, 3, 5, 0, 5),
+    VAR("40_b128_mb2", 40, 4, 2, 128, false, 18, 23680, 2),
+    VAR("40_b128_mb2_fa", 40, 4, 2, 128, true, 18, 23680, 2),
+    VAR("40_b32_mb11", 40, 4, 11, 32, false, 18, 23680, 2),
+    VAR("40_b32_mb11_fa", 40, 4, 11, 32, true, 18, 23680, 2),
+    VAR("40_b64_mb5", 40, 4, 5, 64, false, 18, 23680, 2),
+    VAR("40_b32_mb10", 40, 4, 10, 32, false, 18, 23680, 2),
+    VAR("40_b32_mb12", 40, 4, 12, 32, false, 18, 23680, 2),
+    VAR("48_b128_mb2", 48, 4, 2, 128, false, 20, 4736, 2),
+    VAR("48_b32_mb9", 48, 4, 9, 32, false, 20, 4736, 2),
+    VAR("48_b32_mb9_fa", 48, 4, 9, 32, true, 20, 4736, 2),
+    VAR("48_b32_mb8_fa", 48, 4, 8, 32, true, 20, 4736, 2),
+    VAR("36_b128_mb3", 36, 4, 3, 128, false, 14, 0, 3),
+    VAR("36_b32_mb13", 36, 4, 13, 32, false, 14, 0, 3),
+    VAR("36_b32_mb12_fa", 36, 4, 12, 32, true, 14, 0, 3),
+    VAR("56_b32_mb9_u3", 56, 3, 9, 32, false, 20, 4736, 1),
+    VAR("56_b32_mb8_u4", 56, 4, 8, 32, false, 20, 4736, 1),
+    VAR("63_b32_mb8_u3", 63, 3, 8, 32, false, 20, 4736, 1),
   };
   for (auto& v : vs) {
     bool sel = argc < 2;
