@@ -106,6 +106,16 @@ int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_ch
                         uint64_t chunk_lo, uint64_t nchunks, int policy, uint32_t flags,
                         int device, double* out_chunks, double out_total[2]);
 
+/* Whole walks of `batch` matrices of one order n in one launch (decomposition
+ * leaves, boson-sampling submatrices). cols/x0 hold the
+ * matrices back to back in the pk_dense_f64 layout; out_dd[2*b] is matrix b's
+ * partial over [1, 2^(n-1)-1] (add its g = 0 product and the sign, as
+ * reduce_partials does). One block per matrix at a time, its 2^10 aligned
+ * chunks tree-reduced like a single launch; n < 11 walks one thread per
+ * matrix. */
+int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, int policy,
+                       uint32_t flags, int device, double* out_dd, pk_run_stats* stats);
+
 /* ------------------------------------------------------------- dense complex
  * Interleaved (re, im) doubles: cols[2*(j*n + i) + {0,1}] = a_ij (j < n-1),
  * x0[2*i + {0,1}] = a_{i,n-1} - rowsum_i / 2 (dense_complex_state,

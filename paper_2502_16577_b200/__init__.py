@@ -16,6 +16,7 @@ from .errors import (DecompTimeout, DeviceError, ImpossibleError, ParseError, Pe
 from .generate import (haar_unitary_block, random_binary, random_real, random_sparse_int,
                        random_sparse_real, random_ternary, uniform)
 from .graycode import GrayStep, cbl_sequence, changed_bit, gray_of, subset_columns
+from .batch import permanent_batch
 from .kernels import perm_nw, perm_spa, total_iterates
 from .matrix import (CcsMatrix, CrsMatrix, DenseMatrix, Scalar, SparsePair, coerce_matrix,
                      dense_to_sparse, density, sparse_from_triplets, sparse_to_dense)

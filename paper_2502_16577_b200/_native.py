@@ -81,6 +81,9 @@ SIGNATURES = {
     "pk_dense_c128_chunks": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                             ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _D,
                                             _D]),
+    "pk_dense_f64_batch": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_uint32, ctypes.c_int, _D,
+                                          ctypes.POINTER(RunStats)]),
     "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                               _I32, ctypes.c_int, _U64, ctypes.c_void_p, ctypes.POINTER(RunStats)]),
     "pk_int_ranges": (ctypes.c_int, [_I64, ctypes.c_int, _U64, _U64, ctypes.c_int, ctypes.c_int,

@@ -1,0 +1,76 @@
+"""Many permanents per launch: the caller side of SURVEY.md §8f-2.
+
+permkit evaluates decomposition leaves one by one (preprocess.py:495-504),
+and boson-sampling workloads need the permanents of many n ~ 20-30
+submatrices. ``permanent_batch`` groups the matrices by kind and order and
+walks every real group in ONE launch of ``pk_dense_f64_batch`` (one block per
+matrix at a time, each matrix's aligned chunks tree-reduced exactly like a
+single launch). Complex and integer groups fall back to one device call per
+matrix (still on the GPU).
+"""
+
+from __future__ import annotations
+
+from collections import defaultdict
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .kernels import (DenseF64Problem, _sign_factor, perm_nw, perm_spa, policy_product,
+                      sparse_float_state, total_iterates)
+from .matrix import KIND_REAL, DenseMatrix, SparsePair, coerce_matrix, sparse_to_dense
+from .precision import AccumulatorPolicy, DoubleDouble, as_policy, dd_add
+
+
+def _real_batch(ms: Sequence, policy: AccumulatorPolicy, device: int, exact: bool,
+                stats: Optional[nat.RunStats]) -> List[float]:
+    n = ms[0].n
+    probs = []
+    for m in ms:
+        if isinstance(m, SparsePair):
+            pr = DenseF64Problem(sparse_to_dense(m))
+            pr.x0 = np.ascontiguousarray(sparse_float_state(m)[3], dtype=np.float64)
+        else:
+            pr = DenseF64Problem(m)
+        probs.append(pr)
+    b = len(probs)
+    ncol = (n - 1) * n
+    cols = np.ascontiguousarray(np.concatenate([p.cols[:ncol] for p in probs]) if ncol
+                                else np.zeros(1))
+    x0 = np.ascontiguousarray(np.concatenate([p.x0 for p in probs]))
+    out = np.zeros(2 * b)
+    st = stats if stats is not None else nat.RunStats()
+    rc = nat.load().pk_dense_f64_batch(nat.dptr(cols), nat.dptr(x0), n, b, policy.code,
+                                       nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out), st)
+    nat.check(rc, "pk_dense_f64_batch")
+    res = []
+    for i, p in enumerate(probs):
+        p0 = policy_product(p.x0, policy)
+        acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+        if n > 1:
+            acc = dd_add(acc, DoubleDouble(float(out[2 * i]), float(out[2 * i + 1])))
+        res.append(acc.hi * _sign_factor(n))
+    return res
+
+
+def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = False,
+                    stats: Optional[nat.RunStats] = None) -> list:
+    """Permanents of many matrices; results in input order."""
+    policy = as_policy(policy)
+    ms = [coerce_matrix(m) for m in matrices]
+    out: list = [None] * len(ms)
+    groups = defaultdict(list)
+    for i, m in enumerate(ms):
+        groups[(m.kind, m.n)].append(i)
+    for (kind, n), idx in groups.items():
+        if kind == KIND_REAL:
+            vals = _real_batch([ms[i] for i in idx], policy, device, exact, stats)
+            for i, v in zip(idx, vals):
+                out[i] = v
+        else:
+            for i in idx:
+                m = ms[i]
+                out[i] = (perm_spa(m, policy, devices=[device]) if isinstance(m, SparsePair)
+                          else perm_nw(m, policy, devices=[device]))
+    return out

@@ -284,6 +284,25 @@ int dispatch_dense(int n, const pk::DenseLaunch& a) {
   }
 }
 
+int dispatch_dense_batch(int n, const pk::DenseBatchLaunch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_dense_f64_batch<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40) PK_CASE(41) PK_CASE(42) PK_CASE(43) PK_CASE(44) PK_CASE(45)
+    PK_CASE(46) PK_CASE(47) PK_CASE(48) PK_CASE(49) PK_CASE(50) PK_CASE(51) PK_CASE(52)
+    PK_CASE(53) PK_CASE(54) PK_CASE(55) PK_CASE(56) PK_CASE(57) PK_CASE(58) PK_CASE(59)
+    PK_CASE(60) PK_CASE(61) PK_CASE(62) PK_CASE(63)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
 int dispatch_c128(int n, const pk::C128Launch& a) {
   switch (n) {
 #define PK_CASE(N) \
@@ -963,6 +982,73 @@ int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_
     launch_walk_int(c, ip, d_cols, d_z0, d_s, d_e, nranges, (pk::i192*)c.chunks);
     ck(cudaStreamSynchronize(c.stream), "walker execution");
     ck(cudaMemcpy(out_z, c.chunks, rs.size() * sizeof(pk::i192), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, int policy,
+                       uint32_t flags, int device, double* out_dd, pk_run_stats* stats) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_n(n);
+    check_policy(policy);
+    if (batch < 0) fail(PK_ERR_ARG, "negative batch");
+    if (batch == 0) return;
+    if (!x0 || !out_dd || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
+    const size_t ncol = (size_t)(n > 1 ? n - 1 : 0) * n;
+    DevCtx& c = dev_ctx(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const size_t in_doubles = ncol * batch + (size_t)n * batch;
+    ensure(c.scratch, c.scratch_cap, in_doubles * 8 + 64);
+    double* d_cols = (double*)c.scratch;
+    double* d_x0 = d_cols + ncol * batch;
+    if (ncol) ck(cudaMemcpyAsync(d_cols, cols, ncol * batch * 8, cudaMemcpyHostToDevice, c.stream), "H2D cols");
+    ck(cudaMemcpyAsync(d_x0, x0, (size_t)n * batch * 8, cudaMemcpyHostToDevice, c.stream), "H2D x0");
+    ensure(c.chunks, c.chunks_cap, (size_t)batch);
+    ck(cudaEventRecord(c.e0, c.stream), "event record");
+    int k = 0;
+    if (n >= pk::kDenseNMin) {
+      k = pk::batch_log2_chunk(n, pk::dense_logu(n));
+      const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
+      ensure(c.groups, c.groups_cap, groups * batch);
+      pk::DenseBatchLaunch a{};
+      a.d_cols = d_cols;
+      a.d_x0 = d_x0;
+      a.policy = policy;
+      a.exact = (flags & PK_FLAG_EXACT) != 0;
+      a.batch = batch;
+      a.k = k;
+      a.group_part = c.groups;
+      a.out = c.chunks;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      ck((cudaError_t)dispatch_dense_batch(n, a), "dense_f64 batch launch");
+    } else {
+      const unsigned grid = (unsigned)((batch + pk::kWalkBlock - 1) / pk::kWalkBlock);
+      switch (policy) {
+        case PK_POLICY_DD: pk::walk_dense_f64_multi<pk::POL_DD><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks); break;
+        case PK_POLICY_KAHAN: pk::walk_dense_f64_multi<pk::POL_KAHAN><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks); break;
+        case PK_POLICY_DQ: pk::walk_dense_f64_multi<pk::POL_DQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks); break;
+        default: pk::walk_dense_f64_multi<pk::POL_QQ><<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks); break;
+      }
+      ck(cudaGetLastError(), "walk_dense_f64_multi launch");
+    }
+    ck(cudaEventRecord(c.e1, c.stream), "event record");
+    ck(cudaStreamSynchronize(c.stream), "kernel execution");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c.e0, c.e1), "event time");
+    ck(cudaMemcpy(out_dd, c.chunks, (size_t)batch * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H");
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->kernel_ms = ms;
+      stats->iterates = total_iterates(n) * (uint64_t)batch;
+      stats->log2_chunk = k;
+      stats->devices = 1;
+      stats->launches = 1;
+      stats->chunks = k ? (uint64_t)batch << (n - 1 - k) : 0;
+      stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
   });
 }
 

@@ -66,7 +66,9 @@ __device__ __forceinline__ double row_product(const double (&x)[N]) {
 //   POL  accumulator policy of the per-chunk partial (pk_common.cuh)
 //   PS   product chains (1 = the reference's sequential product, bit exact)
 //   LOGU log2 of the unrolled body length U
-//   CS   where the static steps' column operands come from (below)
+//   (the column operands always come from a shared-memory copy of the
+//    columns read with warp-uniform LDS.128; parameter-bank and hoisted
+//    variants were slower, profiles/r01_k1_variants.md)
 //   BA   block accumulation: sum the U terms of a body in plain double and
 //        fold the body sum once (1 policy fold per U terms instead of per
 //        term). Not bit-identical to the reference's per-term fold.
@@ -75,59 +77,26 @@ __device__ __forceinline__ double row_product(const double (&x)[N]) {
 //        register count is not a divisor-friendly number)
 //   FA   fused accumulate (with BA): the last product multiply and the body
 //        sum become one DFMA, bsum = fma(+-p', x[n-1], bsum)
-template <int POL_, int PS_, int LOGU_, int CS_, bool BA_, int MINB_ = 1, int BLOCK_ = 128,
+template <int POL_, int PS_, int LOGU_, bool BA_, int MINB_ = 1, int BLOCK_ = 128,
           bool FA_ = false>
 struct DenseCfg {
-  static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, CS = CS_, MINB = MINB_;
+  static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, MINB = MINB_;
   static constexpr int BLOCK = BLOCK_;
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
   static constexpr bool FA = FA_ && BA;
 };
-
-// Column-operand sources. Static steps index the columns with compile-time
-// offsets; what ptxas makes of that depends on whether it may hoist:
-//   CS_HOIST  -- plain indexing into the parameter block; ptxas hoists the
-//                body's columns into uniform + vector registers per chunk
-//   CS_RELOAD -- the index carries an opaque, loop-variant zero, so every
-//                body re-reads its columns from the constant bank (LDC)
-//   CS_SMEM   -- columns staged once per block in shared memory, read with
-//                warp-uniform LDS.128 (two doubles per load) every body
-enum ColSrc : int { CS_HOIST = 0, CS_RELOAD = 1, CS_SMEM = 2 };
 
 template <int N>
 __host__ __device__ constexpr int smem_stride() { return (N + 1) & ~1; }
 
 template <int N, class C>
 struct DenseWalk {
-  const DenseF64Params<N>& p;
-  const double* scols;  // shared-memory columns (CS_SMEM), stride smem_stride<N>()
+  const double* scols;  // shared-memory columns, stride smem_stride<N>()
   double x[N];
   Acc<C::POL> acc;
   double bsum;
 
-  __device__ __forceinline__ DenseWalk(const DenseF64Params<N>& p_, const double* s_)
-      : p(p_), scols(s_) {}
-
-  // x[i] += sign * column entry, for a compile-time column J
-  template <int J, int SIGN>  // SIGN: +1, -1, or 0 (= runtime s)
-  __device__ __forceinline__ void update_static(int jz, double s) {
-    if constexpr (C::CS == CS_SMEM) {
-      constexpr int NP = smem_stride<N>();
-      const double2* c2 = reinterpret_cast<const double2*>(scols + (J + jz) * NP);
-#pragma unroll
-      for (int i = 0; i < N; i += 2) {
-        const double2 v = c2[i / 2];
-        x[i] = apply<SIGN>(x[i], v.x, s);
-        if (i + 1 < N) x[i + 1] = apply<SIGN>(x[i + 1], v.y, s);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double c = (C::CS == CS_HOIST) ? p.cols[J * N + i] : p.cols[(J + jz) * N + i];
-        x[i] = apply<SIGN>(x[i], c, s);
-      }
-    }
-  }
+  __device__ __forceinline__ explicit DenseWalk(const double* s_) : scols(s_) {}
 
   template <int SIGN>
   __device__ __forceinline__ static double apply(double xi, double c, double s) {
@@ -136,20 +105,47 @@ struct DenseWalk {
     else return __fma_rn(s, c, xi);  // s = +-1: x + s*c exactly as _loops.py:48
   }
 
-  // runtime column j (uniform in the body's last step, per-chunk at the end)
+  // x[i] += sign * column entry, for a compile-time column J (SIGN 0: run-time s)
+  template <int J, int SIGN>
+  __device__ __forceinline__ void update_static(int jz, double s) {
+    constexpr int NP = smem_stride<N>();
+    const double2* c2 = reinterpret_cast<const double2*>(scols + (J + jz) * NP);
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 v = c2[i / 2];
+      x[i] = apply<SIGN>(x[i], v.x, s);
+      if (i + 1 < N) x[i + 1] = apply<SIGN>(x[i + 1], v.y, s);
+    }
+  }
+
+  // run-time column j (uniform in the body's last step, per-chunk at the end)
   __device__ __forceinline__ void update_dynamic(int j, double s) {
-    if constexpr (C::CS == CS_SMEM) {
-      constexpr int NP = smem_stride<N>();
-      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
+    constexpr int NP = smem_stride<N>();
+    const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
 #pragma unroll
-      for (int i = 0; i < N; i += 2) {
-        const double2 v = c2[i / 2];
-        x[i] = __fma_rn(s, v.x, x[i]);
-        if (i + 1 < N) x[i + 1] = __fma_rn(s, v.y, x[i + 1]);
+    for (int i = 0; i < N; i += 2) {
+      const double2 v = c2[i / 2];
+      x[i] = __fma_rn(s, v.x, x[i]);
+      if (i + 1 < N) x[i + 1] = __fma_rn(s, v.y, x[i + 1]);
+    }
+  }
+
+  // jump-in (init_x_at, parallel.py:162-188): x0 + columns of gray(g_prev), ascending
+  __device__ __forceinline__ void jump_in(const double* x0, uint64_t g_prev) {
+    constexpr int NP = smem_stride<N>();
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x0[i];
+    const uint64_t code = g_prev ^ (g_prev >> 1);
+    for (int j = 0; j < N - 1; ++j) {
+      if ((code >> j) & 1ull) {
+        const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+          const double2 v = c2[i / 2];
+          x[i] = __dadd_rn(x[i], v.x);
+          if (i + 1 < N) x[i + 1] = __dadd_rn(x[i + 1], v.y);
+        }
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = __fma_rn(s, p.cols[j * N + i], x[i]);
     }
   }
 
@@ -211,25 +207,16 @@ struct StaticSteps<N, C, U, U> {
   __device__ __forceinline__ static void run(DenseWalk<N, C>&, double, int) {}
 };
 
-// Walk one aligned chunk; returns its normalised partial (parallel.py:282-289).
+// Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
+// g_end); returns its normalised partial (parallel.py:282-289).
 template <int N, class C>
-__device__ __forceinline__ dd_t walk_chunk(const DenseF64Params<N>& p, const double* scols,
-                                           uint64_t c) {
+__device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0, int k,
+                                           uint64_t g_end, uint64_t c) {
   constexpr int LOGU = C::LOGU;
   constexpr int U = 1 << LOGU;
-  DenseWalk<N, C> w(p, scols);
-  const int k = p.k;
+  DenseWalk<N, C> w(scols);
   const uint64_t base = c << k;
-#pragma unroll
-  for (int i = 0; i < N; ++i) w.x[i] = p.x0[i];
-  // jump-in (init_x_at, parallel.py:162-188): x0 + columns of gray(base), ascending
-  const uint64_t code = base ^ (base >> 1);
-  for (int j = 0; j < N - 1; ++j) {
-    if ((code >> j) & 1ull) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) w.x[i] = __dadd_rn(w.x[i], p.cols[j * N + i]);
-    }
-  }
+  w.jump_in(x0, base);
   const uint64_t nbody = 1ull << (k - LOGU);
   for (uint64_t m = 0; m < nbody; ++m) {
     const uint64_t gb = base + (m << LOGU);
@@ -238,7 +225,7 @@ __device__ __forceinline__ dd_t walk_chunk(const DenseF64Params<N>& p, const dou
     StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
     // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
     const uint64_t g = gb + U;
-    if (m + 1 < nbody || g <= p.g_end) {
+    if (m + 1 < nbody || g <= g_end) {
       const int j = changed_col(g);
       w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
       w.fold(false, false);
@@ -248,24 +235,29 @@ __device__ __forceinline__ dd_t walk_chunk(const DenseF64Params<N>& p, const dou
   return w.acc.partial();
 }
 
+// stage the (N-1) x N columns into shared memory with a stride of
+// smem_stride<N>() doubles (16-byte aligned rows for LDS.128)
+template <int N>
+__device__ __forceinline__ void stage_columns(double* scols, const double* cols) {
+  constexpr int NP = smem_stride<N>();
+  for (int t = threadIdx.x; t < (N - 1) * NP; t += blockDim.x) {
+    const int j = t / NP, i = t % NP;
+    scols[t] = (i < N) ? cols[j * N + i] : 0.0;
+  }
+}
+
 template <int N, class C>
 __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_f64_chunks(const __grid_constant__ DenseF64Params<N> p) {
   extern __shared__ __align__(16) double scols[];
-  if constexpr (C::CS == CS_SMEM) {
-    constexpr int NP = smem_stride<N>();
-    for (int t = threadIdx.x; t < (N - 1) * NP; t += blockDim.x) {
-      const int j = t / NP, i = t % NP;
-      scols[t] = (i < N) ? p.cols[j * N + i] : 0.0;
-    }
-    __syncthreads();
-  }
+  stage_columns<N>(scols, p.cols);
+  __syncthreads();
   const unsigned int lane = threadIdx.x & 31u;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
     const uint64_t c = p.chunk_lo + grp * 32 + lane;
-    dd_t part = walk_chunk<N, C>(p, scols, c);
+    dd_t part = walk_chunk<N, C>(scols, p.x0, p.k, p.g_end, c);
     if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
     part = warp_tree_dd(part);
     if (lane == 0) p.group_part[grp] = part;
@@ -273,9 +265,50 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
   grid_tail_reduce<C::BLOCK>(p.group_part, p.num_groups, p.out, p.counter);
 }
 
-template <int N, class C>
+template <int N>
 __host__ __device__ constexpr size_t dense_smem_bytes() {
-  return C::CS == CS_SMEM ? sizeof(double) * (N - 1) * smem_stride<N>() : 0;
+  return sizeof(double) * (N - 1) * smem_stride<N>();
+}
+
+// ---------------------------------------------------------------------------
+// batched walks: many matrices of one order, one block per matrix at a time
+// (decomposition leaves, boson-sampling submatrices). Each
+// matrix is split into 2^(n-1-k) aligned chunks walked by the block's warps;
+// its partial is the same fixed tree over its groups as a single launch.
+
+template <int N>
+struct DenseBatchParams {
+  const double* cols;   // [batch][(N-1)*N]
+  const double* x0;     // [batch][N]
+  dd_t* group_part;     // [batch][groups] scratch
+  dd_t* out;            // [batch] partial over [1, 2^(N-1)-1]
+  int batch;
+  int k;
+};
+
+template <int N, class C>
+__global__ void __launch_bounds__(C::BLOCK, C::MINB)
+    dense_f64_batch(const __grid_constant__ DenseBatchParams<N> p) {
+  extern __shared__ __align__(16) double smem[];
+  double* scols = smem;
+  double* sx0 = smem + (N - 1) * smem_stride<N>();
+  const uint64_t total = (1ull << (N - 1)) - 1;
+  const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    __syncthreads();
+    stage_columns<N>(scols, p.cols + (size_t)b * (N - 1) * N);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sx0[i] = p.x0[(size_t)b * N + i];
+    __syncthreads();
+    dd_t* gp = p.group_part + (size_t)b * groups;
+    for (int grp = wib; grp < groups; grp += wpb) {
+      dd_t part = walk_chunk<N, C>(scols, sx0, p.k, total, (uint64_t)grp * 32 + lane);
+      part = warp_tree_dd(part);
+      if (lane == 0) gp[grp] = part;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.out[b] = pairwise_fold(gp, 0, groups);
+  }
 }
 
 }  // namespace pk

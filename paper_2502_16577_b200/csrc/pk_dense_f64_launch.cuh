@@ -11,7 +11,7 @@ namespace pk {
 template <int N, class C>
 static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
   auto kern = dense_f64_chunks<N, C>;
-  constexpr size_t smem = dense_smem_bytes<N, C>();
+  constexpr size_t smem = dense_smem_bytes<N>();
   static int occ = -1;  // per instantiation; every B200 gives the same answer
   if (occ < 0) {
     if (smem > 48 * 1024) {
@@ -51,16 +51,61 @@ int launch_dense_f64(const DenseLaunch& a) {
   p.k = a.k;
   switch (a.policy) {
     case POL_DD:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, MB, 128, true>>(a, p);
     case POL_KAHAN:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
+      return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, MB, 128, true>>(a, p);
     case POL_DQ:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, CS_SMEM, true, MB, 128, true>>(a, p);
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, MB, 128, true>>(a, p);
     case POL_QQ:
-      return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, CS_SMEM, false, MB>>(a, p);
+      return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p);
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+template <int N, class C>
+static int launch_batch_cfg(const DenseBatchLaunch& a) {
+  auto kern = dense_f64_batch<N, C>;
+  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N;
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
+    if (e != cudaSuccess) return (int)e;
+    occ = o > 0 ? o : 1;
+  }
+  DenseBatchParams<N> p;
+  p.cols = a.d_cols;
+  p.x0 = a.d_x0;
+  p.group_part = a.group_part;
+  p.out = a.out;
+  p.batch = a.batch;
+  p.k = a.k;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if ((uint64_t)a.batch < grid) grid = a.batch;
+  kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_dense_f64_batch(const DenseBatchLaunch& a) {
+  constexpr int LOGU = dense_logu(N);
+  constexpr int MB = dense_minb(N);
+  switch (a.policy) {
+    case POL_DD:
+      return a.exact ? launch_batch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a)
+                     : launch_batch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, MB, 128, true>>(a);
+    case POL_KAHAN:
+      return a.exact ? launch_batch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a)
+                     : launch_batch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, MB, 128, true>>(a);
+    case POL_DQ:
+      return a.exact ? launch_batch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a)
+                     : launch_batch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, MB, 128, true>>(a);
+    case POL_QQ:
+      return launch_batch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a);
     default:
       return (int)cudaErrorInvalidValue;
   }
@@ -68,4 +113,6 @@ int launch_dense_f64(const DenseLaunch& a) {
 
 }  // namespace pk
 
-#define PK_INSTANTIATE_DENSE_F64(N) template int pk::launch_dense_f64<N>(const pk::DenseLaunch&);
+#define PK_INSTANTIATE_DENSE_F64(N)                                 \
+  template int pk::launch_dense_f64<N>(const pk::DenseLaunch&); \
+  template int pk::launch_dense_f64_batch<N>(const pk::DenseBatchLaunch&);

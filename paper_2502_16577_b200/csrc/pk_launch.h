@@ -39,6 +39,28 @@ struct DenseLaunch {
 template <int N>
 int launch_dense_f64(const DenseLaunch& a);
 
+// batched whole walks of `batch` matrices of order N (device inputs)
+struct DenseBatchLaunch {
+  const double* d_cols;  // [batch][(N-1)*N]
+  const double* d_x0;    // [batch][N]
+  int policy;
+  bool exact;
+  int batch;
+  int k;
+  dd_t* group_part;      // [batch][2^(N-1-k)/32]
+  dd_t* out;             // [batch]
+  cudaStream_t stream;
+  int sms;
+};
+
+// chunk exponent of a batched walk: at most 2^10 chunks per matrix
+constexpr int batch_log2_chunk(int N, int logu) {
+  return (N - 1 - 10) > (logu + 1) ? (N - 1 - 10) : (logu + 1);
+}
+
+template <int N>
+int launch_dense_f64_batch(const DenseBatchLaunch& a);
+
 // complex: register kernels for N in [kC128NMin, kC128NMax]; cols/x0 are
 // interleaved (re, im); cols must already be on the device (d_cols)
 constexpr int kC128NMin = 11;

@@ -56,6 +56,28 @@ __global__ void __launch_bounds__(kWalkBlock)
   out[r] = acc.partial();
 }
 
+// whole walks of `batch` small matrices, one thread per matrix: matrix r has
+// columns cols + r*(n-1)*n and seed x0 + r*n (batched API for n < 11)
+template <int POL>
+__global__ void __launch_bounds__(kWalkBlock)
+    walk_dense_f64_multi(const double* __restrict__ cols, const double* __restrict__ x0, int n,
+                         int batch, dd_t* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= batch) return;
+  const double* cr = cols + (size_t)r * (n - 1) * n;
+  double x[64];
+  for (int i = 0; i < n; ++i) x[i] = x0[(size_t)r * n + i];
+  Acc<POL> acc;
+  const uint64_t end = (1ull << (n - 1)) - 1;
+  for (uint64_t g = 1; g <= end; ++g) {
+    const int j = changed_col(g);
+    const double s = flip_on(g, j) ? 1.0 : -1.0;
+    for (int i = 0; i < n; ++i) x[i] = __fma_rn(s, cr[j * n + i], x[i]);
+    walk_fold_real<POL>(acc, x, n, (g & 1ull) != 0);
+  }
+  out[r] = end ? acc.partial() : dd_t{0.0, 0.0};
+}
+
 // sparse real, CCS: cptrs[n+1], rids[nnz], vals[nnz]
 template <int POL>
 __global__ void __launch_bounds__(kWalkBlock)

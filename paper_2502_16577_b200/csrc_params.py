@@ -1,0 +1,14 @@
+"""Mirror of the compile-time tuning in csrc/pk_launch.h (kept in sync by
+tests/test_host.py::test_csrc_params_mirror)."""
+
+
+def dense_logu(n: int) -> int:
+    return 4 if n <= 50 else 3
+
+
+def dense_minb(n: int) -> int:
+    return 3 if n <= 36 else 2
+
+
+def batch_log2_chunk(n: int, logu: int) -> int:
+    return max(n - 1 - 10, logu + 1)

@@ -1,0 +1,51 @@
+"""Batched walks (pk_dense_f64_batch): one launch for many matrices must give
+each matrix exactly what a single launch with the same chunking gives."""
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+import paper_2502_16577_b200 as pk
+from paper_2502_16577_b200 import _native
+from paper_2502_16577_b200.csrc_params import batch_log2_chunk, dense_logu
+from paper_2502_16577_b200.kernels import DenseF64Problem, policy_product, _sign_factor
+from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_add
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [11, 16, 20, 24])
+@pytest.mark.parametrize("policy", ["dd", "kahan", "qq"])
+def test_batch_equals_single_launch_bitwise(n, policy):
+    pol = AccumulatorPolicy.parse(policy)
+    ms = [pk.random_real(n, 100 + s, 0.0, 1.0) for s in range(7)]
+    got = pk.permanent_batch(ms, policy)
+    k = batch_log2_chunk(n, dense_logu(n))
+    for m, g in zip(ms, got):
+        prob = DenseF64Problem(m)
+        part = prob.walk(1, pk.total_iterates(n), pol, log2_chunk=k)
+        p0 = policy_product(prob.x0, pol)
+        acc = dd_add(p0 if isinstance(p0, DoubleDouble) else DoubleDouble(p0, 0.0), part)
+        assert g == acc.hi * _sign_factor(n)
+
+
+def test_small_orders_match_reference_bitwise(golden):
+    case = next(c for c in golden["cases"] if c["name"] == "real_rand8")
+    m = pk.DenseMatrix.from_array(gio.dense_array(case))
+    for ch in case["chunked"]:
+        if ch["tau"] == 1:
+            assert pk.permanent_batch([m, m], ch["policy"])[1].hex() == ch["value"]
+
+
+def test_mixed_batch_and_throughput_stats():
+    ms = [pk.random_real(22, s, 0.0, 1.0) for s in range(300)]
+    ms += [pk.uniform(16, 0.91), pk.DenseMatrix.from_rows([[1, 2], [3, 4]]),
+           pk.haar_unitary_block(12, 1), pk.random_real(5, 1)]
+    st = _native.RunStats()
+    got = pk.permanent_batch(ms, "kahan", stats=st)
+    assert got[301] == 10 and isinstance(got[302], complex)
+    import math
+    assert abs(got[300] - math.factorial(16) * 0.91 ** 16) <= 1e-12 * got[300]
+    for i in (0, 150, 299):
+        assert abs(got[i] - pk.perm_nw(ms[i], "kahan")) <= 1e-11 * abs(got[i])
+    assert st.launches == 1 and st.iterates > 0

@@ -164,3 +164,14 @@ def test_partials_file_round_trip(tmp_path):
     bad.write_text("# nope\n" + path.read_text())
     with pytest.raises(pk.ParseError):
         pk.read_partials_file(bad)
+
+
+def test_csrc_params_mirror():
+    import re
+    from paper_2502_16577_b200 import csrc_params as cp
+    text = open(os.path.join(ROOT, "paper_2502_16577_b200", "csrc", "pk_launch.h")).read()
+    assert "constexpr int dense_logu(int N) { return N <= 50 ? 4 : 3; }" in text
+    assert "constexpr int dense_minb(int N) { return N <= 36 ? 3 : 2; }" in text
+    assert "(N - 1 - 10) > (logu + 1) ? (N - 1 - 10) : (logu + 1)" in text
+    assert cp.dense_logu(50) == 4 and cp.dense_logu(51) == 3
+    assert cp.batch_log2_chunk(20, 4) == 9 and cp.batch_log2_chunk(12, 4) == 5

@@ -54,7 +54,7 @@ struct Host {
 template <int N, class C>
 void run_variant(const char* name, Host<N>& h, int k, unsigned long long groups_limit, int reps) {
   auto kern = dense_f64_chunks<N, C>;
-  const size_t smem = dense_smem_bytes<N, C>();
+  const size_t smem = dense_smem_bytes<N>();
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaFuncAttributes fa;
   CK(cudaFuncGetAttributes(&fa, kern));
@@ -126,7 +126,7 @@ int main(int argc, char** argv) {
   static Host<24> h24;
   struct V { const char* name; void (*fn)(); };
 #define VAR(NM, NN, UX, MB, BL, FA, KK, GL, R) \
-  V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, CS_SMEM, true, MB, BL, FA>>(NM, h##NN, KK, GL, R); }}
+  V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, BL, FA>>(NM, h##NN, KK, GL, R); }}
   std::vector<V> vs = {
     VAR("40_b128_mb2", 40, 4, 2, 128, false, 18, 23680, 2),
     VAR("40_b128_mb2_fa", 40, 4, 2, 128, true, 18, 23680, 2),
