@@ -53,6 +53,9 @@ extern "C" {
 #define PK_FLAG_EXACT 1u /* per-chunk arithmetic identical to the reference loop
                             (one policy fold per term); default folds a body
                             of 16 terms in plain double first */
+#define PK_FLAG_SPARSE 2u /* integer walks: generate, compile (NVRTC) and cache a
+                             per-matrix SpaRyser kernel that updates only the
+                             flipped column's nonzeros (_loops.py:263-284) */
 
 typedef struct pk_run_stats {
   double kernel_ms;       /* device time of the call's kernels, max over devices */
@@ -156,9 +159,12 @@ typedef struct pk_int_info {
   double log2_term_bound; /* log2 of that product */
 } pk_int_info;
 
-int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, int log2_chunk,
+int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, uint32_t flags, int log2_chunk,
            const int* devices, int ndev, uint64_t out_z[3], pk_int_info* info,
            pk_run_stats* stats);
+/* the CUDA source of the generated SpaRyser kernel for `a` (n >= 11): copies
+ * at most cap-1 bytes + NUL into buf, *len = full length */
+int pk_int_spa_source(const int64_t* a, int n, char* buf, uint64_t cap, uint64_t* len);
 /* one exact partial per range (walkers, one device thread each): 3 words each */
 int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_t* ends,
                   int nranges, int device, uint64_t* out_z, pk_int_info* info);

@@ -31,6 +31,7 @@ PK_ERR_CUDA = 5
 PK_ERR_OVERFLOW = 6
 
 PK_FLAG_EXACT = 1
+PK_FLAG_SPARSE = 2
 
 
 class RunStats(ctypes.Structure):
@@ -84,8 +85,11 @@ SIGNATURES = {
     "pk_dense_f64_batch": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_uint32, ctypes.c_int, _D,
                                           ctypes.POINTER(RunStats)]),
-    "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
-                              _I32, ctypes.c_int, _U64, ctypes.c_void_p, ctypes.POINTER(RunStats)]),
+    "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                              ctypes.c_int, _I32, ctypes.c_int, _U64, ctypes.c_void_p,
+                              ctypes.POINTER(RunStats)]),
+    "pk_int_spa_source": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_char_p, ctypes.c_uint64,
+                                         _U64]),
     "pk_int_ranges": (ctypes.c_int, [_I64, ctypes.c_int, _U64, _U64, ctypes.c_int, ctypes.c_int,
                                      _U64, ctypes.c_void_p]),
 }

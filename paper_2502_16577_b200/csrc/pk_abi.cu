@@ -18,6 +18,7 @@
 #include "pk_launch.h"
 #include "pk_walker.cuh"
 #include "pk_int.cuh"
+#include "pk_spa.h"
 #include <cmath>
 #include <functional>
 
@@ -618,6 +619,8 @@ struct IntPrep {
   double log2_bound = 0.0;
   std::vector<int> zcols;  // (n-1)*n, z-space column steps
   std::vector<int> z0;
+  std::vector<int64_t> zmax;  // per-row bound on |z_i|
+  bool sparse = false;        // walk with the generated SpaRyser kernel
 };
 
 // y = 2x state of kernels.py:104-110, rescaled per row (pk_int.cuh header)
@@ -626,6 +629,7 @@ IntPrep prep_int(const int64_t* a, int n) {
   ip.n = n;
   ip.zcols.assign((size_t)(n > 1 ? n - 1 : 1) * n, 0);
   ip.z0.assign(n, 0);
+  ip.zmax.assign(n, 0);
   const __int128 lim = ((__int128)1 << 31) - 1;
   int64_t zmax_all = 0;
   double lb = 0.0;
@@ -648,6 +652,7 @@ IntPrep prep_int(const int64_t* a, int n) {
       const __int128 v = a[(size_t)i * n + j];
       ip.zcols[(size_t)j * n + i] = (int)(even ? v : 2 * v);
     }
+    ip.zmax[i] = (int64_t)zmax;
     if (zmax > zmax_all) zmax_all = (int64_t)zmax;
     if (zmax == 0) zero_row = true;
     else lb += std::log2((double)zmax);
@@ -744,7 +749,29 @@ void run_int_on_device(int dev, const IntPrep& ip, const DensePlan& pl, uint64_t
     const int* d_cols = upload_int(c, ip, pieces, &d_s, &d_e, &d_z0);
     ck(cudaEventRecord(c.e0, c.stream), "event record");
     // i192 buffers are carved from the dd workspaces (24 B <= 32 B per dd pair)
-    if (g_cnt > 0) {
+    if (g_cnt > 0 && ip.sparse) {
+      ensure(c.groups, c.groups_cap, g_cnt);
+      pk::SpaIntSpec sp;
+      sp.n = ip.n;
+      sp.zcols = ip.zcols;
+      sp.zmax = ip.zmax;
+      pk::SpaIntLaunch a{};
+      a.d_cols = d_cols;
+      a.d_z0 = d_z0;
+      a.group_part = c.groups;
+      a.out = c.out;
+      a.counter = c.counter;
+      a.chunk_lo = pl.chunk_lo + 32 * g_lo;
+      a.num_groups = g_cnt;
+      a.g_end = g_end;
+      a.k = pl.k;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      std::string err;
+      const int rc = pk::spa_int_launch(sp, a, err);
+      if (rc != 0) fail(PK_ERR_CUDA, err);
+      ++r.launches;
+    } else if (g_cnt > 0) {
       ensure(c.groups, c.groups_cap, g_cnt);
       pk::IntLaunch a{};
       a.d_cols = d_cols;
@@ -903,7 +930,7 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
   });
 }
 
-int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, int log2_chunk,
+int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, uint32_t flags, int log2_chunk,
            const int* devices, int ndev, uint64_t out_z[3], pk_int_info* info,
            pk_run_stats* stats) {
   return guarded([&] {
@@ -912,9 +939,10 @@ int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, int log2_chunk
     if (!a || !out_z) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
     IntPrep ip = prep_int(a, n);
+    ip.sparse = (flags & PK_FLAG_SPARSE) != 0 && n >= pk::kIntNMin;
     fill_info(ip, info);
     std::vector<int> devs = device_list(devices, ndev);
-    const int logu = n >= pk::kIntNMin ? pk::int_logu(n) : 0;
+    const int logu = n >= pk::kIntNMin ? (ip.sparse ? pk::kSpaLogU : pk::int_logu(n)) : 0;
     DensePlan pl = plan_dense(n, logu, start, end, log2_chunk, (int)devs.size());
     const int nd = pl.num_groups ? (int)devs.size() : 1;
     std::vector<IntDevResult> res(nd);
@@ -1048,6 +1076,26 @@ int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, i
       stats->chunks = k ? (uint64_t)batch << (n - 1 - k) : 0;
       stats->wall_ms =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+int pk_int_spa_source(const int64_t* a, int n, char* buf, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    check_n(n);
+    if (!a || !len) fail(PK_ERR_ARG, "null pointer argument");
+    if (n < pk::kIntNMin) fail(PK_ERR_ARG, "SpaRyser kernels need n >= 11");
+    IntPrep ip = prep_int(a, n);
+    pk::SpaIntSpec sp;
+    sp.n = n;
+    sp.zcols = ip.zcols;
+    sp.zmax = ip.zmax;
+    const std::string src = pk::spa_int_source(sp);
+    *len = src.size();
+    if (buf && cap > 0) {
+      const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;
+      std::memcpy(buf, src.data(), m);
+      buf[m] = '\0';
     }
   });
 }

@@ -49,6 +49,19 @@ def _signed(words, bits: int) -> int:
     return v - (1 << bits) if v >> (bits - 1) else v
 
 
+SPARSE_MIN_N = 36
+
+
+def spa_source(m) -> str:
+    """CUDA source of the generated SpaRyser kernel for an integer matrix."""
+    prob = IntProblem(m)
+    ln = ctypes.c_uint64(0)
+    buf = ctypes.create_string_buffer(1 << 22)
+    rc = nat.load().pk_int_spa_source(prob._a(), prob.n, buf, 1 << 22, ctypes.byref(ln))
+    nat.check(rc, "pk_int_spa_source")
+    return buf.value.decode()
+
+
 class IntProblem:
     def __init__(self, m):
         dense = sparse_to_dense(m) if isinstance(m, SparsePair) else m
@@ -64,13 +77,19 @@ class IntProblem:
         return self.a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
 
     def walk(self, start: int, end: int, devices=None, log2_chunk: int = 0,
-             stats: Optional[nat.RunStats] = None) -> Tuple[List[int], IntInfo]:
+             stats: Optional[nat.RunStats] = None,
+             sparse: Optional[bool] = None) -> Tuple[List[int], IntInfo]:
+        """sparse=None picks the generated SpaRyser kernel for n >= SPARSE_MIN_N
+        (its one-off NVRTC compile, ~1 s, then pays for itself)."""
         lib = nat.load()
         out = np.zeros(3, dtype=np.uint64)
         dptr, nd, _keep = nat.devices_arg(devices)
         st = stats if stats is not None else nat.RunStats()
-        rc = lib.pk_int(self._a(), self.n, start, end, log2_chunk, dptr, nd, nat.u64ptr(out),
-                        ctypes.byref(self.info), st)
+        if sparse is None:
+            sparse = self.n >= SPARSE_MIN_N
+        flags = nat.PK_FLAG_SPARSE if sparse else 0
+        rc = lib.pk_int(self._a(), self.n, start, end, flags, log2_chunk, dptr, nd,
+                        nat.u64ptr(out), ctypes.byref(self.info), st)
         nat.check(rc, "pk_int")
         return [int(w) for w in out], self.info
 

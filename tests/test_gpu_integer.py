@@ -118,3 +118,27 @@ def test_large_terms_refuse_instead_of_rounding():
         pk.run_range(m, 1, 100)
     with pytest.raises(OverflowError):
         pk.perm_nw(m)
+
+
+@pytest.mark.parametrize("n,density", [(14, 0.3), (20, 0.25), (24, 0.4), (26, 0.15)])
+def test_generated_spa_kernel_is_exact(n, density):
+    # per-matrix NVRTC SpaRyser kernel vs the template register kernel vs the
+    # walkers, on whole walks and on an unaligned range
+    for seed in (1, 2):
+        m = pk.random_binary(n, seed, density)
+        prob = IntProblem(m)
+        T = pk.total_iterates(n)
+        a, info = prob.walk(1, T, sparse=True)
+        b, _ = prob.walk(1, T, sparse=False)
+        assert a == b
+        s, e = 3 + T // 5, T - 7
+        a, _ = prob.walk(s, e, sparse=True)
+        w, _ = prob.ranges([(s, e)])
+        assert a == w[0]
+
+
+def test_sparse_general_integers():
+    m = pk.random_sparse_int(22, 0.3, 4)
+    prob = IntProblem(m)
+    T = pk.total_iterates(22)
+    assert prob.walk(1, T, sparse=True)[0] == prob.walk(1, T, sparse=False)[0]

@@ -175,3 +175,22 @@ def test_csrc_params_mirror():
     assert "(N - 1 - 10) > (logu + 1) ? (N - 1 - 10) : (logu + 1)" in text
     assert cp.dense_logu(50) == 4 and cp.dense_logu(51) == 3
     assert cp.batch_log2_chunk(20, 4) == 9 and cp.batch_log2_chunk(12, 4) == 5
+
+
+def test_generated_spa_source_compiles_for_sm100a(tmp_path):
+    # the per-matrix SpaRyser kernel source is valid CUDA for sm_100a and
+    # updates only the nonzeros of each statically known column
+    import subprocess
+    from paper_2502_16577_b200.integer import spa_source
+    m = pk.random_binary(24, 3, 0.2)
+    src = spa_source(m)
+    assert "spa_int" in src and "switch (j)" in src
+    nnz_col0 = sum(1 for i in range(24) if m.entry(i, 0))
+    body = src.split("const int smid")[1].split("{", 1)[1].split("int g0")[0]
+    assert body.count("z") == nnz_col0
+    f = tmp_path / "spa.cu"
+    f.write_text(src)
+    r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-gencode",
+                        "arch=compute_100a,code=sm_100a", "-cubin", "-o", str(tmp_path / "spa.cubin"),
+                        str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
