@@ -315,7 +315,7 @@ int spa_int_launch(const SpaIntSpec& sp, const SpaIntLaunch& a, std::string& err
         return (int)cudaErrorInvalidSource;
       }
       const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
-                            "--extra-device-vectorization", "-lineinfo"};
+                            "--device-int128", "-lineinfo"};
       const int rc = nv.compile(prog, 5, opts);
       if (rc != 0) {
         size_t ls = 0;

@@ -30,11 +30,21 @@ def test_batch_equals_single_launch_bitwise(n, policy):
 
 
 def test_small_orders_match_reference_bitwise(golden):
+    # n < 11 walks one thread per matrix over [1, 2^(n-1)-1]: the reference's
+    # run_range over that range reduced with its g = 0 term
+    from paper_2502_16577_b200.parallel import PartialResult
     case = next(c for c in golden["cases"] if c["name"] == "real_rand8")
     m = pk.DenseMatrix.from_array(gio.dense_array(case))
-    for ch in case["chunked"]:
-        if ch["tau"] == 1:
-            assert pk.permanent_batch([m, m], ch["policy"])[1].hex() == ch["value"]
+    T = pk.total_iterates(8)
+    for r in case["ranges"]:
+        if (r["start"], r["end"]) != (1, T):
+            continue
+        pol = r["policy"]
+        p0 = case["p0"][pol]
+        p0 = DoubleDouble(*gio.dec_dd(p0)) if pol == "qq" else float.fromhex(p0)
+        part = PartialResult(0, 1, T, T, "real64", DoubleDouble(*gio.dec_dd(r["value"])))
+        want = pk.reduce_partials([part], p0, 8)
+        assert pk.permanent_batch([m, m], pol)[1] == want
 
 
 def test_mixed_batch_and_throughput_stats():
