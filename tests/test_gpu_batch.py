@@ -52,10 +52,12 @@ def test_mixed_batch_and_throughput_stats():
     ms += [pk.uniform(16, 0.91), pk.DenseMatrix.from_rows([[1, 2], [3, 4]]),
            pk.haar_unitary_block(12, 1), pk.random_real(5, 1)]
     st = _native.RunStats()
-    got = pk.permanent_batch(ms, "kahan", stats=st)
+    got = pk.permanent_batch(ms, "dd", stats=st)
     assert got[301] == 10 and isinstance(got[302], complex)
     import math
     assert abs(got[300] - math.factorial(16) * 0.91 ** 16) <= 1e-12 * got[300]
     for i in (0, 150, 299):
         assert abs(got[i] - pk.perm_nw(ms[i], "kahan")) <= 1e-11 * abs(got[i])
+    with pytest.raises(pk.PolicyError):  # complex members keep the DD-only rule
+        pk.permanent_batch([pk.haar_unitary_block(12, 1)], "kahan")
     assert st.launches == 1 and st.iterates > 0
