@@ -51,8 +51,9 @@ struct Host {
   }
 };
 
-template <int N, class C>
+template <int N, class C, bool SPLIT = false>
 void run_variant(const char* name, Host<N>& h, int k, unsigned long long groups_limit, int reps) {
+  static_assert(!SPLIT, "the lane-pair split variant was retired (profiles/r01_k1_variants.md)");
   auto kern = dense_f64_chunks<N, C>;
   const size_t smem = dense_smem_bytes<N>();
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -68,7 +69,7 @@ void run_variant(const char* name, Host<N>& h, int k, unsigned long long groups_
   if (groups_limit && groups > groups_limit) groups = groups_limit;
   DenseF64Params<N> p = h.p;
   dd_t *gp, *out; unsigned int* ctr;
-  CK(cudaMalloc(&gp, groups * sizeof(dd_t)));
+  CK(cudaMalloc(&gp, 2 * groups * sizeof(dd_t)));
   CK(cudaMalloc(&out, sizeof(dd_t)));
   CK(cudaMalloc(&ctr, sizeof(unsigned)));
   CK(cudaMemset(ctr, 0, sizeof(unsigned)));
@@ -127,24 +128,12 @@ int main(int argc, char** argv) {
   struct V { const char* name; void (*fn)(); };
 #define VAR(NM, NN, UX, MB, BL, FA, KK, GL, R) \
   V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, BL, FA>>(NM, h##NN, KK, GL, R); }}
+#define SVAR(NM, NN, UX, MB, KK, GL, R) \
+  V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, 128, true>, true>(NM, h##NN, KK, GL, R); }}
   std::vector<V> vs = {
-    VAR("40_b128_mb2", 40, 4, 2, 128, false, 18, 23680, 2),
-    VAR("40_b128_mb2_fa", 40, 4, 2, 128, true, 18, 23680, 2),
-    VAR("40_b32_mb11", 40, 4, 11, 32, false, 18, 23680, 2),
-    VAR("40_b32_mb11_fa", 40, 4, 11, 32, true, 18, 23680, 2),
-    VAR("40_b64_mb5", 40, 4, 5, 64, false, 18, 23680, 2),
-    VAR("40_b32_mb10", 40, 4, 10, 32, false, 18, 23680, 2),
-    VAR("40_b32_mb12", 40, 4, 12, 32, false, 18, 23680, 2),
-    VAR("48_b128_mb2", 48, 4, 2, 128, false, 20, 4736, 2),
-    VAR("48_b32_mb9", 48, 4, 9, 32, false, 20, 4736, 2),
-    VAR("48_b32_mb9_fa", 48, 4, 9, 32, true, 20, 4736, 2),
-    VAR("48_b32_mb8_fa", 48, 4, 8, 32, true, 20, 4736, 2),
-    VAR("36_b128_mb3", 36, 4, 3, 128, false, 14, 0, 3),
-    VAR("36_b32_mb13", 36, 4, 13, 32, false, 14, 0, 3),
-    VAR("36_b32_mb12_fa", 36, 4, 12, 32, true, 14, 0, 3),
-    VAR("56_b32_mb9_u3", 56, 3, 9, 32, false, 20, 4736, 1),
-    VAR("56_b32_mb8_u4", 56, 4, 8, 32, false, 20, 4736, 1),
-    VAR("63_b32_mb8_u3", 63, 3, 8, 32, false, 20, 4736, 1),
+    VAR("40_k1_fa", 40, 4, 2, 128, true, 18, 23680, 2),
+    VAR("48_k1_fa", 48, 4, 2, 128, true, 20, 4736, 2),
+    VAR("36_k1_fa", 36, 4, 3, 128, true, 14, 0, 3),
   };
   for (auto& v : vs) {
     bool sel = argc < 2;
