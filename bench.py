@@ -43,10 +43,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="dense", choices=["dense", "binary", "haar"],
+    ap.add_argument("--workload", default="dense", choices=["dense", "binary", "haar", "sparse"],
                     help="dense: n x n random [0,1) real (the metric's workload); binary: "
                          "n x n 0/1 density 0.3, exact (config 3); haar: n x n block of a "
-                         "Haar unitary, complex (config 4)")
+                         "Haar unitary, complex (config 4); sparse: n x n random [0,1) real with "
+                         "density 0.3 (SpaRyser, generated nonzero-only kernel)")
     ap.add_argument("--n", type=int, default=0, help="order (default 40 / 40 / 32)")
     ap.add_argument("--policy", default="kahan")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -277,7 +278,7 @@ class Workload:
         self.kind = args.workload
         self.n = args.n or (32 if self.kind == "haar" else 40)
         n = self.n
-        self.policy = args.policy if self.kind == "dense" else "dd"
+        self.policy = args.policy if self.kind in ("dense", "sparse") else "dd"
         if self.kind == "dense":
             self.rows = matrix_rows(n)
             self.m = pk.DenseMatrix.from_rows(self.rows)
@@ -291,6 +292,17 @@ class Workload:
             self.flops = None
             self.desc = (f"n={n} sparse 0/1 matrix density 0.3 seed {SEED} (SpaRyser, exact "
                          f"int), whole walk per step")
+        elif self.kind == "sparse":
+            d = pk.random_sparse_real(n, 0.3, SEED, 0.0, 1.0)
+            self.m = d
+            self.rows = pk.sparse_to_dense(d).rows()
+            # 2 flops per stored nonzero of the flipped column (weighted by how
+            # often column j flips, 2^-(j+1)) + n for the product
+            nnz = [int(d.ccs.cptrs[j + 1] - d.ccs.cptrs[j]) for j in range(n - 1)]
+            self.flops = n + 2 * sum(c * 2.0 ** -(j + 1) for j, c in enumerate(nnz))
+            self.desc = (f"n={n} sparse real fp64, random [0,1) entries at density 0.3 seed "
+                         f"{SEED}, policy {self.policy} (SpaRyser: generated kernel updates only "
+                         f"the flipped column's nonzeros), whole walk per step")
         else:
             self.m = pk.haar_unitary_block(n, SEED)
             self.rows = self.m.rows()
@@ -307,6 +319,11 @@ class Workload:
             from paper_2502_16577_b200.kernels import DenseF64Problem
             p = DenseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
                                             devices=devices, stats=st)
+            return [p.hi, p.lo], st
+        if self.kind == "sparse":
+            from paper_2502_16577_b200.kernels import SparseF64Problem
+            p = SparseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
+                                             devices=devices, stats=st)
             return [p.hi, p.lo], st
         if self.kind == "haar":
             from paper_2502_16577_b200.complex_walk import DenseC128Problem
@@ -325,8 +342,10 @@ class Workload:
         from paper_2502_16577_b200.precision import (AccumulatorPolicy, DoubleDouble, dd_add,
                                                      dd_pairwise)
         n = self.n
-        if self.kind == "dense":
-            p0 = policy_product(DenseF64Problem(self.m).x0, AccumulatorPolicy.parse(self.policy))
+        if self.kind in ("dense", "sparse"):
+            from paper_2502_16577_b200.kernels import SparseF64Problem
+            prob = DenseF64Problem(self.m) if self.kind == "dense" else SparseF64Problem(self.m)
+            p0 = policy_product(prob.x0, AccumulatorPolicy.parse(self.policy))
             acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
             acc = dd_add(acc, dd_pairwise([tuple(g[:2]) for g in gathered]))
             return (acc.hi * _sign_factor(n)).hex()
@@ -353,9 +372,33 @@ class Workload:
         n = self.n
         if self.kind == "dense":
             return 2 * ((n - 1) * n * 8 + n * 8)  # kernel parameter block + workspace copy
+        if self.kind == "sparse":
+            nnz = int(self.m.ccs.cptrs[n - 1])  # dense columns + packed nonzeros + seed
+            return (n - 1) * n * 8 + n * 8 + nnz * 8
         if self.kind == "haar":
             return (n - 1) * n * 16 + 2 * n * 16
         return (n - 1) * n * 4 + n * 4
+
+
+# ncu --set full summaries of each workload's dominant kernel (profiles/):
+# dram__bytes_read.sum + dram__bytes_write.sum of one launch
+NCU_SUMMARY = {"dense": "r01_ncu_k1_full_summary.csv", "sparse": "r01_ncu_spa_f64_full_summary.csv"}
+
+
+def ncu_traffic(kind):
+    """(bytes per launch, source) from the committed ncu summary, or (None, None)."""
+    name = NCU_SUMMARY.get(kind)
+    path = os.path.join(ROOT, "profiles", name) if name else None
+    if not path or not os.path.exists(path):
+        return None, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    import csv
+    with open(path) as f:
+        for row in csv.DictReader(f):
+            if row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(row["value"]) * scale.get(row["unit"], 1.0)
+    return total, "profiles/" + name
 
 
 def run_b200(args, dist: Dist):
@@ -435,8 +478,12 @@ def run_b200(args, dist: Dist):
         pass
     if wl.flops:
         achieved_tf = wl.flops * (total / N) / (statistics.mean(step_k) * 1e-3) * 1e-12
+        traffic, tsrc = ncu_traffic(wl.kind)
         roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": achieved_tf / peak_tf, "traffic": None,
+                    "frac": achieved_tf / peak_tf, "traffic": traffic,
+                    "traffic_source": (f"DRAM bytes per launch of the same kernel from ncu --set "
+                                       f"full ({tsrc}); the walk reads only its <32 KB inputs"
+                                       if tsrc else None),
                     "note": f"algorithmic {wl.flops} flop/update x updates per launch / CUDA-event "
                             "time of that launch; peak = live DFMA microbenchmark (pk_fp64_peak); "
                             "MEASURED_PEAKS.json has no FP64 entry (hbm_gbs=%s, bf16_tflops=%s); "
@@ -463,7 +510,7 @@ def run_b200(args, dist: Dist):
         "vs_baseline": ups / PAPER_N40_UPS if (n == 40 and wl.kind == "dense") else None,
         "vs_baseline_ref": "SUperman best kernel on a Quadro GV100, n=40 in 14.17 s "
                            "(PAPER.md:785) = 3.88e10 updates/s",
-        "dtype": {"dense": "f64", "haar": "c128 (f64 pairs)", "binary": "int32 state, exact "
+        "dtype": {"dense": "f64", "sparse": "f64", "haar": "c128 (f64 pairs)", "binary": "int32 state, exact "
                   "int128 products, 192-bit sums"}[wl.kind],
         "data": "synthetic",
         "config": {"workload": wl.desc, "n": n, "policy": wl.policy,

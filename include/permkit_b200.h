@@ -53,7 +53,7 @@ extern "C" {
 #define PK_FLAG_EXACT 1u /* per-chunk arithmetic identical to the reference loop
                             (one policy fold per term); default folds a body
                             of 16 terms in plain double first */
-#define PK_FLAG_SPARSE 2u /* integer walks: generate, compile (NVRTC) and cache a
+#define PK_FLAG_SPARSE 2u /* real and integer walks: generate, compile (NVRTC) and cache a
                              per-matrix SpaRyser kernel that updates only the
                              flipped column's nonzeros (_loops.py:263-284) */
 
@@ -118,6 +118,25 @@ int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_ch
  * matrix. */
 int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, int policy,
                        uint32_t flags, int device, double* out_dd, pk_run_stats* stats);
+
+/* --------------------------------------------------------------- sparse real
+ * SpaRyser (chunk_sparse_f64, _loops.py:110-183; state of sparse_float_state,
+ * kernels.py:113-127): CCS of the whole matrix, cptrs[n+1] / rids / vals as
+ * the reference's CcsMatrix (rows strictly ascending within a column, else
+ * PK_ERR_STRUCTURE); column n-1 is already folded into x0 by the caller.
+ * The aligned middle of [start, end] runs a kernel generated and compiled
+ * (NVRTC, cached per pattern and device) for the nonzero pattern: each step
+ * adds only the flipped column's nonzeros. Same arithmetic, chunking and
+ * reduction as pk_dense_f64 on the densified matrix, hence the same bits.
+ * pk_dense_f64 / pk_dense_f64_chunks with PK_FLAG_SPARSE do the same for a
+ * dense column array (pattern = its nonzero entries). */
+int pk_sparse_f64(const int64_t* cptrs, const int64_t* rids, const double* vals, int n,
+                  const double* x0, uint64_t start, uint64_t end, int policy, uint32_t flags,
+                  int log2_chunk, const int* devices, int ndev, double out_dd[2],
+                  pk_run_stats* stats);
+/* the generated CUDA source for the nonzero pattern of `cols` (n >= 11) */
+int pk_spa_f64_source(const double* cols, int n, int policy, uint32_t flags, char* buf,
+                      uint64_t cap, uint64_t* len);
 
 /* ------------------------------------------------------------- dense complex
  * Interleaved (re, im) doubles: cols[2*(j*n + i) + {0,1}] = a_ij (j < n-1),

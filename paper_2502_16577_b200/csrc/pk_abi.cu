@@ -21,6 +21,7 @@
 #include "pk_spa.h"
 #include <cmath>
 #include <functional>
+#include <memory>
 
 namespace {
 
@@ -322,7 +323,8 @@ int dispatch_c128(int n, const pk::C128Launch& a) {
 
 size_t ncols_of(int n) { return (size_t)(n > 1 ? n - 1 : 1) * n; }
 
-Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact) {
+Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact,
+                    bool sparse = false) {
   Kind kd;
   kd.n = n;
   kd.streams = 1;
@@ -333,6 +335,47 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 8);
   const double* h_cols = cols;
   const double* h_x0 = x0;
+  if (sparse && n >= pk::kDenseNMin) {
+    // SpaRyser: generated kernel over the nonzero pattern of the columns;
+    // packed nonzero values appended to the inputs (16-byte aligned)
+    auto sp = std::make_shared<pk::SpaF64Spec>();
+    sp->n = n;
+    sp->policy = policy;
+    sp->exact = exact;
+    sp->rows.resize(n - 1);
+    for (int j = 0; j < n - 1; ++j)
+      for (int i = 0; i < n; ++i)
+        if (cols[(size_t)j * n + i] != 0.0) sp->rows[j].push_back(i);
+    int nv = 0;
+    const std::vector<int> off = pk::spa_f64_offsets(*sp, &nv);
+    const size_t voff = (kd.input.size() + 1) & ~size_t(1);
+    kd.input.resize(voff + nv, 0.0);
+    for (int j = 0; j < n - 1; ++j)
+      for (size_t t = 0; t < sp->rows[j].size(); ++t)
+        kd.input[voff + off[j] + t] = cols[(size_t)j * n + sp->rows[j][t]];
+    kd.logu = pk::spa_f64_logu(n);
+    kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                  uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+      pk::SpaF64Launch a{};
+      a.d_cols = d_in;
+      a.d_x0 = d_in + nc;
+      a.d_vals = d_in + voff;
+      a.group_part = gparts;
+      a.chunk_part = cparts;
+      a.out = out;
+      a.counter = c.counter;
+      a.chunk_lo = chunk_lo;
+      a.num_groups = groups;
+      a.g_end = g_end;
+      a.k = k;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      std::string err;
+      const int rc = pk::spa_f64_launch(*sp, a, err);
+      if (rc != 0) fail(PK_ERR_CUDA, err);
+      return 0;
+    };
+  } else {
   kd.fast = [=](DevCtx& c, const double*, uint64_t chunk_lo, uint64_t groups, uint64_t g_end,
                 int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
     pk::DenseLaunch a{};
@@ -352,6 +395,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     a.sms = c.sms;
     return dispatch_dense(n, a);
   };
+  }
   kd.walk = [=](DevCtx& c, const double* d_in, const unsigned long long* d_s,
                 const unsigned long long* d_e, int nr, dd_t* out) {
     const double* d_cols = d_in;
@@ -828,6 +872,30 @@ void fill_info(const IntPrep& ip, pk_int_info* info) {
 // ===========================================================================
 // exported C ABI
 
+namespace {
+// CCS (cptrs[n+1], rids, vals) -> dense (n-1) x n toggled columns; the
+// reference's StructureError conditions (matrix.py:198-222, :256-259)
+std::vector<double> ccs_to_cols(const int64_t* cptrs, const int64_t* rids, const double* vals,
+                                int n, int comps) {
+  if (!cptrs || (cptrs[n] > 0 && (!rids || !vals))) fail(PK_ERR_ARG, "null pointer argument");
+  if (cptrs[0] != 0) fail(PK_ERR_STRUCTURE, "cptrs[0] must be 0");
+  std::vector<double> cols(ncols_of(n) * comps, 0.0);
+  for (int j = 0; j < n; ++j) {
+    if (cptrs[j + 1] < cptrs[j]) fail(PK_ERR_STRUCTURE, "cptrs must be non-decreasing");
+    for (int64_t t = cptrs[j]; t < cptrs[j + 1]; ++t) {
+      const int64_t r = rids[t];
+      if (r < 0 || r >= n) fail(PK_ERR_STRUCTURE, "row index out of range");
+      if (t > cptrs[j] && rids[t - 1] >= r)
+        fail(PK_ERR_STRUCTURE, "row indices must be strictly ascending within a column");
+      if (j < n - 1)
+        for (int q = 0; q < comps; ++q) cols[((size_t)j * n + r) * comps + q] = vals[t * comps + q];
+    }
+  }
+  return cols;
+}
+
+}  // namespace
+
 extern "C" {
 
 int pk_abi_version(void) { return PK_ABI_VERSION; }
@@ -848,7 +916,8 @@ int pk_dense_f64(const double* cols, const double* x0, int n, uint64_t start, ui
     check_policy(policy);
     if (!x0 || !out_dd || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
-    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0);
+    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0,
+                             (flags & PK_FLAG_SPARSE) != 0);
     dd_t out[2];
     drive(kd, start, end, log2_chunk, device_list(devices, ndev), out, stats);
     out_dd[0] = out[0].hi;
@@ -877,7 +946,8 @@ int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_ch
     check_n(n);
     check_policy(policy);
     if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
-    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0);
+    Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0,
+                             (flags & PK_FLAG_SPARSE) != 0);
     dd_t tot[2];
     drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
     out_total[0] = tot[0].hi;
@@ -1091,6 +1161,49 @@ int pk_int_spa_source(const int64_t* a, int n, char* buf, uint64_t cap, uint64_t
     sp.zcols = ip.zcols;
     sp.zmax = ip.zmax;
     const std::string src = pk::spa_int_source(sp);
+    *len = src.size();
+    if (buf && cap > 0) {
+      const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;
+      std::memcpy(buf, src.data(), m);
+      buf[m] = '\0';
+    }
+  });
+}
+
+int pk_sparse_f64(const int64_t* cptrs, const int64_t* rids, const double* vals, int n,
+                  const double* x0, uint64_t start, uint64_t end, int policy, uint32_t flags,
+                  int log2_chunk, const int* devices, int ndev, double out_dd[2],
+                  pk_run_stats* stats) {
+  return guarded([&] {
+    check_n(n);
+    check_policy(policy);
+    if (!x0 || !out_dd) fail(PK_ERR_ARG, "null pointer argument");
+    check_range(n, start, end);
+    const std::vector<double> cols = ccs_to_cols(cptrs, rids, vals, n, 1);
+    Kind kd = dense_f64_kind(cols.data(), x0, n, policy, (flags & PK_FLAG_EXACT) != 0, true);
+    dd_t out[2];
+    drive(kd, start, end, log2_chunk, device_list(devices, ndev), out, stats);
+    out_dd[0] = out[0].hi;
+    out_dd[1] = out[0].lo;
+  });
+}
+
+int pk_spa_f64_source(const double* cols, int n, int policy, uint32_t flags, char* buf,
+                      uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    check_n(n);
+    check_policy(policy);
+    if (!cols || !len) fail(PK_ERR_ARG, "null pointer argument");
+    if (n < pk::kDenseNMin) fail(PK_ERR_ARG, "SpaRyser kernels need n >= 11");
+    pk::SpaF64Spec sp;
+    sp.n = n;
+    sp.policy = policy;
+    sp.exact = (flags & PK_FLAG_EXACT) != 0;
+    sp.rows.resize(n - 1);
+    for (int j = 0; j < n - 1; ++j)
+      for (int i = 0; i < n; ++i)
+        if (cols[(size_t)j * n + i] != 0.0) sp.rows[j].push_back(i);
+    const std::string src = pk::spa_f64_source(sp);
     *len = src.size();
     if (buf && cap > 0) {
       const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;

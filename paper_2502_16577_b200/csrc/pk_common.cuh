@@ -7,7 +7,15 @@
 // (/root/reference/pkg/src/permkit/_loops.py:35-107) when the product is
 // evaluated sequentially.
 #pragma once
+#if defined(__CUDACC_RTC__)
+// NVRTC (generated SpaRyser kernels, pk_spa_codegen.cu) has no system headers
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+#else
 #include <cstdint>
+#endif
 
 namespace pk {
 

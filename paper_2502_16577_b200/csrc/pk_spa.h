@@ -34,6 +34,44 @@ int spa_int_launch(const SpaIntSpec& sp, const SpaIntLaunch& a, std::string& err
 // the generated CUDA source (diagnostics / tests)
 std::string spa_int_source(const SpaIntSpec& sp);
 
+// ------------------------------------------------------------- sparse real
+// Per-pattern generated kernel for the sparse fp64 walk (chunk_sparse_f64,
+// _loops.py:110-183): x[n] in registers, each step adds only the flipped
+// column's nonzeros (values staged in shared memory, positions literal).
+// Arithmetic, chunking and reduction are K1's (pk_dense_f64.cuh), so the
+// result is bit-identical to K1 on the densified matrix.
+struct SpaF64Spec {
+  int n = 0;
+  std::vector<std::vector<int>> rows;  // rows[j]: nonzero rows of column j < n-1, ascending
+  int policy = 0;                      // pk::Policy
+  bool exact = false;                  // per-term fold (PK_FLAG_EXACT)
+};
+
+// packed value layout: column j's nonzeros at [off[j], off[j] + rows[j].size()),
+// every column starting at an even offset (LDS.128 pairs)
+std::vector<int> spa_f64_offsets(const SpaF64Spec& sp, int* total);
+
+struct SpaF64Launch {
+  const double* d_cols;  // device dense (n-1)*n columns (jump-in)
+  const double* d_x0;    // device seed x0[n]
+  const double* d_vals;  // device packed nonzeros (spa_f64_offsets layout)
+  void* group_part;      // device dd_t [num_groups]
+  void* chunk_part;      // device dd_t [num_groups*32] or null
+  void* out;             // device dd_t [1]
+  unsigned int* counter;
+  uint64_t chunk_lo;
+  uint64_t num_groups;
+  uint64_t g_end;
+  int k;
+  cudaStream_t stream;
+  int sms;
+};
+
+int spa_f64_launch(const SpaF64Spec& sp, const SpaF64Launch& a, std::string& err);
+std::string spa_f64_source(const SpaF64Spec& sp);
+// body length (log2) of the generated sparse real kernel for order n
+constexpr int spa_f64_logu(int n) { return n <= 50 ? 4 : 3; }
+
 // body length of the generated kernels (8 steps)
 constexpr int kSpaLogU = 3;
 

@@ -19,6 +19,8 @@ from __future__ import annotations
 
 from typing import List, Optional, Sequence, Tuple, Union
 
+import ctypes
+
 import numpy as np
 
 from . import _native as nat
@@ -180,6 +182,8 @@ class DenseF64Problem:
         nat.check(rc, "pk_dense_f64_ranges")
         return [DoubleDouble(float(out[2 * i]), float(out[2 * i + 1])) for i in range(len(spans))]
 
+    flags = 0  # PK_FLAG_SPARSE for the SpaRyser subclass
+
     def chunks(self, log2_chunk: int, chunk_lo: int, nchunks: int, policy: AccumulatorPolicy,
                exact: bool = True, device: int = 0):
         """Per-chunk partials of the register kernel (parity diagnostics)."""
@@ -188,10 +192,54 @@ class DenseF64Problem:
         tot = np.zeros(2)
         rc = lib.pk_dense_f64_chunks(nat.dptr(self.cols), nat.dptr(self.x0), self.n, log2_chunk,
                                      chunk_lo, nchunks, policy.code,
-                                     nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out),
-                                     nat.dptr(tot))
+                                     self.flags | (nat.PK_FLAG_EXACT if exact else 0), device,
+                                     nat.dptr(out), nat.dptr(tot))
         nat.check(rc, "pk_dense_f64_chunks")
         return out.reshape(-1, 2), DoubleDouble(float(tot[0]), float(tot[1]))
+
+
+class SparseF64Problem(DenseF64Problem):
+    """Marshalled sparse real walk (SpaRyser): the reference's CCS state
+    (sparse_float_state, kernels.py:113-127) for pk_sparse_f64, whose aligned
+    middle runs a kernel generated for the nonzero pattern (each step adds
+    only the flipped column's nonzeros, _loops.py:122-124). Range walkers and
+    the bit-exact paths use the densified columns (x + 0.0 == x)."""
+
+    flags = nat.PK_FLAG_SPARSE
+
+    def __init__(self, s: SparsePair):
+        super().__init__(sparse_to_dense(s))
+        cptrs, rids, vals, x0 = sparse_float_state(s)
+        self.cptrs = np.ascontiguousarray(cptrs, dtype=np.int64)
+        self.rids = np.ascontiguousarray(rids if len(rids) else np.zeros(1), dtype=np.int64)
+        self.vals = np.ascontiguousarray(vals if len(vals) else np.zeros(1), dtype=np.float64)
+        self.x0 = np.ascontiguousarray(x0, dtype=np.float64)
+
+    def walk(self, start: int, end: int, policy: AccumulatorPolicy, *, exact: bool = False,
+             devices: Optional[Sequence[int]] = None, log2_chunk: int = 0,
+             stats: Optional[nat.RunStats] = None) -> DoubleDouble:
+        lib = nat.load()
+        out = np.zeros(2)
+        dptr, nd, _keep = nat.devices_arg(devices)
+        st = stats if stats is not None else nat.RunStats()
+        rc = lib.pk_sparse_f64(nat.i64ptr(self.cptrs), nat.i64ptr(self.rids), nat.dptr(self.vals),
+                               self.n, nat.dptr(self.x0), start, end, policy.code,
+                               nat.PK_FLAG_EXACT if exact else 0, log2_chunk, dptr, nd,
+                               nat.dptr(out), st)
+        nat.check(rc, "pk_sparse_f64")
+        return DoubleDouble(float(out[0]), float(out[1]))
+
+    def source(self, policy: AccumulatorPolicy, exact: bool = False) -> str:
+        """CUDA source of the generated kernel for this pattern (diagnostics)."""
+        lib = nat.load()
+        ln = np.zeros(1, dtype=np.uint64)
+        flags = nat.PK_FLAG_EXACT if exact else 0
+        nat.check(lib.pk_spa_f64_source(nat.dptr(self.cols), self.n, policy.code, flags, None, 0,
+                                        nat.u64ptr(ln)), "pk_spa_f64_source")
+        buf = ctypes.create_string_buffer(int(ln[0]) + 1)
+        nat.check(lib.pk_spa_f64_source(nat.dptr(self.cols), self.n, policy.code, flags, buf,
+                                        len(buf), nat.u64ptr(ln)), "pk_spa_f64_source")
+        return buf.value.decode()
 
 
 def _real_walk_total(a: DenseMatrix, policy: AccumulatorPolicy, devices=None,
@@ -235,17 +283,12 @@ def perm_spa(s: SparsePair, policy: "AccumulatorPolicy | str" = AccumulatorPolic
             raise PolicyError("complex matrices support the plain-double policy only")
         from .complex_walk import complex_walk_total
         return complex_walk_total(s, devices=devices)
-    # x + s*0 == x, so the dense walk over the densified pair performs the
-    # sparse walk's arithmetic exactly; the seed uses the sparse row sums
     return _real_walk_total_sparse(s, policy, devices)
 
 
 def _real_walk_total_sparse(s: SparsePair, policy, devices) -> float:
     n = s.n
-    dense = sparse_to_dense(s)
-    prob = DenseF64Problem(dense)
-    _, _, _, x0 = sparse_float_state(s)
-    prob.x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    prob = SparseF64Problem(s)
     p0 = policy_product(prob.x0, policy)
     acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
     if n > 1:

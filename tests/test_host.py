@@ -8,6 +8,8 @@ import ctypes
 import os
 import re
 
+import numpy as np
+
 import pytest
 
 import paper_2502_16577_b200 as pk
@@ -194,3 +196,29 @@ def test_generated_spa_source_compiles_for_sm100a(tmp_path):
                         "arch=compute_100a,code=sm_100a", "-cubin", "-o", str(tmp_path / "spa.cubin"),
                         str(f)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("n,exact", [(40, False), (40, True), (24, False)])
+def test_generated_spa_f64_source_compiles_without_spills(tmp_path, n, exact):
+    # the per-pattern sparse real kernel is valid sm_100a CUDA against the
+    # same device headers the nvcc-built kernels use, touches only the
+    # nonzeros of each static column, and keeps x[n] in registers (no spills)
+    import subprocess
+    from paper_2502_16577_b200 import kernels as K
+    from paper_2502_16577_b200.precision import AccumulatorPolicy
+    rng = np.random.default_rng(n)
+    a = rng.uniform(size=(n, n)) * (rng.uniform(size=(n, n)) < 0.3)
+    trip = [(i, j, float(a[i, j])) for i in range(n) for j in range(n) if a[i, j] != 0.0]
+    prob = K.SparseF64Problem(pk.sparse_from_triplets(n, trip, "real64"))
+    src = prob.source(AccumulatorPolicy.KAHAN, exact=exact)
+    assert "spa_f64" in src and "switch (j)" in src
+    step1 = src.split("// step 1: column 0")[1].split("// step 2")[0]
+    assert step1.count("__dadd_rn(x") + step1.count("__dsub_rn(x") == int((a[:, 0] != 0).sum())
+    f = tmp_path / "spa_f64.cu"
+    f.write_text(src)
+    csrc = os.path.join(ROOT, "paper_2502_16577_b200", "csrc")
+    r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-gencode",
+                        "arch=compute_100a,code=sm_100a", "-cubin", "-I", csrc, "-Xptxas", "-v",
+                        "-o", str(tmp_path / "spa.cubin"), str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "0 bytes spill stores" in r.stderr and "0 bytes spill loads" in r.stderr, r.stderr
