@@ -159,6 +159,19 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
                          uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
                          double* out_chunks, double out_total[4]);
 
+/* SpaRyser for complex pairs (chunk_sparse_c128, _loops.py:212-235; state of
+ * sparse_complex_state, kernels.py:130-143): vals interleaved (re, im) per
+ * stored entry, otherwise as pk_sparse_f64. out as pk_dense_c128. The
+ * generated kernel keeps K3's arithmetic, body length and reduction, so the
+ * result equals pk_dense_c128 on the densified pair bit for bit.
+ * pk_dense_c128 / pk_dense_c128_chunks accept PK_FLAG_SPARSE likewise. */
+int pk_sparse_c128(const int64_t* cptrs, const int64_t* rids, const double* vals, int n,
+                   const double* x0, uint64_t start, uint64_t end, uint32_t flags,
+                   int log2_chunk, const int* devices, int ndev, double out[4],
+                   pk_run_stats* stats);
+int pk_spa_c128_source(const double* cols, int n, uint32_t flags, char* buf, uint64_t cap,
+                       uint64_t* len);
+
 /* --------------------------------------------------------- exact integers
  * a: row-major n*n int64 matrix (integer kind, matrix.py:53-63). The walk
  * runs on z_i = y_i / 2 (even row sum) or y_i (odd row sum), y = 2x the

@@ -90,6 +90,11 @@ SIGNATURES = {
                                      _I32, ctypes.c_int, _D, ctypes.POINTER(RunStats)]),
     "pk_spa_f64_source": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
                                          ctypes.c_char_p, ctypes.c_uint64, _U64]),
+    "pk_sparse_c128": (ctypes.c_int, [_I64, _I64, _D, ctypes.c_int, _D, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _I32,
+                                      ctypes.c_int, _D, ctypes.POINTER(RunStats)]),
+    "pk_spa_c128_source": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_uint32, ctypes.c_char_p,
+                                          ctypes.c_uint64, _U64]),
     "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                               ctypes.c_int, _I32, ctypes.c_int, _U64, ctypes.c_void_p,
                               ctypes.POINTER(RunStats)]),

@@ -1,9 +1,11 @@
 """Complex (boson-sampling) walks on the GPU: dense complex register kernels
 (csrc/pk_dense_c128.cuh, 11 <= n <= 40) and complex range walkers.
 
-Sparse complex pairs run as their densified twin with the sparse seed: the
-dense walk adds s*0 for absent entries, which leaves x unchanged, so the
-arithmetic is the reference's sparse loop (_loops.py:212-235).
+Sparse complex pairs (SpaRyser, _loops.py:212-235) go through
+pk_sparse_c128: the aligned middle of a walk runs a kernel generated for the
+pair's nonzero pattern (each step updates only the flipped column's
+nonzeros) with K3's arithmetic; range walkers and exact paths use the
+densified columns with the sparse seed (x + 0 == x).
 """
 
 from __future__ import annotations
@@ -20,10 +22,15 @@ from .precision import DoubleDouble, dd_add
 
 class DenseC128Problem:
     def __init__(self, m):
-        if isinstance(m, SparsePair):
+        self.sparse = isinstance(m, SparsePair)
+        if self.sparse:
             dense = sparse_to_dense(m)
             cols, _ = dense_complex_state(dense)
-            x0 = sparse_complex_state(m)[3]
+            cptrs, rids, vals, x0 = sparse_complex_state(m)
+            self.cptrs = np.ascontiguousarray(cptrs, dtype=np.int64)
+            self.rids = np.ascontiguousarray(rids if len(rids) else np.zeros(1), dtype=np.int64)
+            v = np.ascontiguousarray(vals if len(vals) else np.zeros(1), dtype=np.complex128)
+            self.vals = np.ascontiguousarray(v.view(np.float64))
             self.n = m.n
         else:
             cols, x0 = dense_complex_state(m)
@@ -40,10 +47,16 @@ class DenseC128Problem:
         out = np.zeros(4)
         dptr, nd, _keep = nat.devices_arg(devices)
         st = stats if stats is not None else nat.RunStats()
-        rc = lib.pk_dense_c128(nat.dptr(self.cols), nat.dptr(self.x0), self.n, start, end,
-                               nat.PK_FLAG_EXACT if exact else 0, log2_chunk, dptr, nd,
-                               nat.dptr(out), st)
-        nat.check(rc, "pk_dense_c128")
+        flags = nat.PK_FLAG_EXACT if exact else 0
+        if self.sparse:
+            rc = lib.pk_sparse_c128(nat.i64ptr(self.cptrs), nat.i64ptr(self.rids),
+                                    nat.dptr(self.vals), self.n, nat.dptr(self.x0), start, end,
+                                    flags, log2_chunk, dptr, nd, nat.dptr(out), st)
+            nat.check(rc, "pk_sparse_c128")
+        else:
+            rc = lib.pk_dense_c128(nat.dptr(self.cols), nat.dptr(self.x0), self.n, start, end,
+                                   flags, log2_chunk, dptr, nd, nat.dptr(out), st)
+            nat.check(rc, "pk_dense_c128")
         return DoubleDouble(out[0], out[1]), DoubleDouble(out[2], out[3])
 
     def ranges(self, spans: Sequence[Tuple[int, int]], device: int = 0) -> List[complex]:
@@ -64,11 +77,25 @@ class DenseC128Problem:
         lib = nat.load()
         out = np.zeros(2 * nchunks)
         tot = np.zeros(4)
+        flags = (nat.PK_FLAG_EXACT if exact else 0) | (nat.PK_FLAG_SPARSE if self.sparse else 0)
         rc = lib.pk_dense_c128_chunks(nat.dptr(self.cols), nat.dptr(self.x0), self.n, log2_chunk,
-                                      chunk_lo, nchunks, nat.PK_FLAG_EXACT if exact else 0,
-                                      device, nat.dptr(out), nat.dptr(tot))
+                                      chunk_lo, nchunks, flags, device, nat.dptr(out),
+                                      nat.dptr(tot))
         nat.check(rc, "pk_dense_c128_chunks")
         return out.reshape(-1, 2), (DoubleDouble(tot[0], tot[1]), DoubleDouble(tot[2], tot[3]))
+
+    def source(self, exact: bool = False) -> str:
+        """CUDA source of the generated SpaRyser kernel for this pattern."""
+        import ctypes
+        lib = nat.load()
+        ln = np.zeros(1, dtype=np.uint64)
+        flags = nat.PK_FLAG_EXACT if exact else 0
+        nat.check(lib.pk_spa_c128_source(nat.dptr(self.cols), self.n, flags, None, 0,
+                                         nat.u64ptr(ln)), "pk_spa_c128_source")
+        buf = ctypes.create_string_buffer(int(ln[0]) + 1)
+        nat.check(lib.pk_spa_c128_source(nat.dptr(self.cols), self.n, flags, buf, len(buf),
+                                         nat.u64ptr(ln)), "pk_spa_c128_source")
+        return buf.value.decode()
 
     def p0(self) -> complex:
         p = complex(1.0)

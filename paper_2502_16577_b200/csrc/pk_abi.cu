@@ -420,7 +420,21 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
   return kd;
 }
 
-Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact) {
+pk::SpaC128Spec spa_c128_spec(const double* cols, int n, bool exact) {
+  pk::SpaC128Spec sp;
+  sp.n = n;
+  sp.exact = exact;
+  sp.rows.resize(n - 1);
+  for (int j = 0; j < n - 1; ++j)
+    for (int i = 0; i < n; ++i) {
+      const double* v = cols + 2 * ((size_t)j * n + i);
+      if (v[0] != 0.0 || v[1] != 0.0) sp.rows[j].push_back(i);
+    }
+  return sp;
+}
+
+Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
+                     bool sparse = false) {
   Kind kd;
   kd.n = n;
   kd.streams = 2;
@@ -430,6 +444,38 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact) {
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 16);
   const double* h_x0 = x0;
+  if (sparse && kd.logu > 0) {
+    // SpaRyser: generated kernel over the nonzero pattern; packed nonzeros
+    // (interleaved re, im) appended to the inputs
+    auto sp = std::make_shared<pk::SpaC128Spec>(spa_c128_spec(cols, n, exact));
+    const size_t voff = kd.input.size();
+    for (int j = 0; j < n - 1; ++j)
+      for (int r : sp->rows[j]) {
+        kd.input.push_back(cols[2 * ((size_t)j * n + r)]);
+        kd.input.push_back(cols[2 * ((size_t)j * n + r) + 1]);
+      }
+    kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                  uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+      pk::SpaC128Launch a{};
+      a.d_cols = d_in;
+      a.d_x0 = d_in + nc;
+      a.d_vals = d_in + voff;
+      a.group_part = gparts;
+      a.chunk_part = cparts;
+      a.out = out;
+      a.counter = c.counter;
+      a.chunk_lo = chunk_lo;
+      a.num_groups = groups;
+      a.g_end = g_end;
+      a.k = k;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      std::string err;
+      const int rc = pk::spa_c128_launch(*sp, a, err);
+      if (rc != 0) fail(PK_ERR_CUDA, err);
+      return 0;
+    };
+  } else {
   kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                 uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
     pk::C128Launch a{};
@@ -448,6 +494,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact) {
     a.sms = c.sms;
     return dispatch_c128(n, a);
   };
+  }
   kd.walk = [=](DevCtx& c, const double* d_in, const unsigned long long* d_s,
                 const unsigned long long* d_e, int nr, dd_t* out) {
     const unsigned grid = (unsigned)((nr + pk::kWalkBlock - 1) / pk::kWalkBlock);
@@ -962,7 +1009,8 @@ int pk_dense_c128(const double* cols, const double* x0, int n, uint64_t start, u
     check_n(n);
     if (!x0 || !out || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
-    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0);
+    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0,
+                              (flags & PK_FLAG_SPARSE) != 0);
     dd_t res[2];
     drive(kd, start, end, log2_chunk, device_list(devices, ndev), res, stats);
     out[0] = res[0].hi;
@@ -990,7 +1038,8 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
   return guarded([&] {
     check_n(n);
     if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
-    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0);
+    Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0,
+                              (flags & PK_FLAG_SPARSE) != 0);
     dd_t tot[2];
     drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
     out_total[0] = tot[0].hi;
@@ -1204,6 +1253,42 @@ int pk_spa_f64_source(const double* cols, int n, int policy, uint32_t flags, cha
       for (int i = 0; i < n; ++i)
         if (cols[(size_t)j * n + i] != 0.0) sp.rows[j].push_back(i);
     const std::string src = pk::spa_f64_source(sp);
+    *len = src.size();
+    if (buf && cap > 0) {
+      const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;
+      std::memcpy(buf, src.data(), m);
+      buf[m] = '\0';
+    }
+  });
+}
+
+int pk_sparse_c128(const int64_t* cptrs, const int64_t* rids, const double* vals, int n,
+                   const double* x0, uint64_t start, uint64_t end, uint32_t flags,
+                   int log2_chunk, const int* devices, int ndev, double out[4],
+                   pk_run_stats* stats) {
+  return guarded([&] {
+    check_n(n);
+    if (!x0 || !out) fail(PK_ERR_ARG, "null pointer argument");
+    check_range(n, start, end);
+    const std::vector<double> cols = ccs_to_cols(cptrs, rids, vals, n, 2);
+    Kind kd = dense_c128_kind(cols.data(), x0, n, (flags & PK_FLAG_EXACT) != 0, true);
+    dd_t o[2];
+    drive(kd, start, end, log2_chunk, device_list(devices, ndev), o, stats);
+    out[0] = o[0].hi;
+    out[1] = o[0].lo;
+    out[2] = o[1].hi;
+    out[3] = o[1].lo;
+  });
+}
+
+int pk_spa_c128_source(const double* cols, int n, uint32_t flags, char* buf, uint64_t cap,
+                       uint64_t* len) {
+  return guarded([&] {
+    check_n(n);
+    if (!cols || !len) fail(PK_ERR_ARG, "null pointer argument");
+    if (n < pk::kC128NMin || n > pk::kC128NMax)
+      fail(PK_ERR_ARG, "complex SpaRyser kernels need 11 <= n <= 40");
+    const std::string src = pk::spa_c128_source(spa_c128_spec(cols, n, (flags & PK_FLAG_EXACT) != 0));
     *len = src.size();
     if (buf && cap > 0) {
       const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;

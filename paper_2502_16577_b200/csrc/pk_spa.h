@@ -72,6 +72,35 @@ std::string spa_f64_source(const SpaF64Spec& sp);
 // body length (log2) of the generated sparse real kernel for order n
 constexpr int spa_f64_logu(int n) { return n <= 50 ? 4 : 3; }
 
+// ---------------------------------------------------------- sparse complex
+// Per-pattern generated kernel for the sparse complex walk (chunk_sparse_c128,
+// _loops.py:212-235) with K3's arithmetic, body length and reduction
+// (pk_dense_c128.cuh): bit-identical to K3 on the densified pair.
+struct SpaC128Spec {
+  int n = 0;
+  std::vector<std::vector<int>> rows;  // nonzero rows of column j < n-1
+  bool exact = false;
+};
+
+struct SpaC128Launch {
+  const double* d_cols;  // device dense interleaved (n-1)*n complex columns (jump-in)
+  const double* d_x0;    // device interleaved seed
+  const double* d_vals;  // device packed interleaved nonzeros, column by column
+  void* group_part;      // device dd_t [2*num_groups]
+  void* chunk_part;      // device dd_t [num_groups*32] or null
+  void* out;             // device dd_t [2]
+  unsigned int* counter;
+  uint64_t chunk_lo;
+  uint64_t num_groups;
+  uint64_t g_end;
+  int k;
+  cudaStream_t stream;
+  int sms;
+};
+
+int spa_c128_launch(const SpaC128Spec& sp, const SpaC128Launch& a, std::string& err);
+std::string spa_c128_source(const SpaC128Spec& sp);
+
 // body length of the generated kernels (8 steps)
 constexpr int kSpaLogU = 3;
 

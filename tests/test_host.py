@@ -222,3 +222,23 @@ def test_generated_spa_f64_source_compiles_without_spills(tmp_path, n, exact):
                         "-o", str(tmp_path / "spa.cubin"), str(f)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "0 bytes spill stores" in r.stderr and "0 bytes spill loads" in r.stderr, r.stderr
+
+
+@pytest.mark.parametrize("n,exact", [(32, False), (40, True)])
+def test_generated_spa_c128_source_compiles_without_spills(tmp_path, n, exact):
+    import subprocess
+    from paper_2502_16577_b200.complex_walk import DenseC128Problem
+    rng = np.random.default_rng(n)
+    a = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))) * (rng.uniform(size=(n, n)) < 0.3)
+    trip = [(i, j, complex(a[i, j])) for i in range(n) for j in range(n) if a[i, j] != 0]
+    src = DenseC128Problem(pk.sparse_from_triplets(n, trip, "complex128")).source(exact)
+    step1 = src.split("// step 1: column 0")[1].split("// step 2")[0].split("const u64 g = gb")[0]
+    assert step1.count("const double2 v = sv2[") == int((a[:, 0] != 0).sum())
+    f = tmp_path / "spa_c128.cu"
+    f.write_text(src)
+    csrc = os.path.join(ROOT, "paper_2502_16577_b200", "csrc")
+    r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-gencode",
+                        "arch=compute_100a,code=sm_100a", "-cubin", "-I", csrc, "-Xptxas", "-v",
+                        "-o", str(tmp_path / "spa.cubin"), str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "0 bytes spill stores" in r.stderr, r.stderr
