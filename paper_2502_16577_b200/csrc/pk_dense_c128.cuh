@@ -37,10 +37,14 @@ struct DenseC128Params {
   int k;
 };
 
-template <int LOGU_, bool EXACT_, int MINB_>
+// FA (fast mode): the last complex multiply of each product and the body sum
+// fold into four DFMAs, b += (+-p) * x[N-1] per component (two FP64
+// instructions fewer per update)
+template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false>
 struct C128Cfg {
   static constexpr int LOGU = LOGU_, MINB = MINB_;
   static constexpr bool EXACT = EXACT_;
+  static constexpr bool FA = FA_ && !EXACT_;
 };
 
 // complex partial sum: plain (reference) or compensated per component
@@ -141,6 +145,28 @@ struct C128Walk {
   }
 
   __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
+    if constexpr (C::FA) {
+      double pr = xr[0], pi = xi[0];
+#pragma unroll
+      for (int i = 1; i < N - 1; ++i) {
+        const double r = __fma_rn(pr, xr[i], -__dmul_rn(pi, xi[i]));
+        const double m = __fma_rn(pr, xi[i], __dmul_rn(pi, xr[i]));
+        pr = r;
+        pi = m;
+      }
+      if (odd) {
+        pr = -pr;
+        pi = -pi;
+      }
+      if (first_in_body) {
+        br = __fma_rn(pr, xr[N - 1], -__dmul_rn(pi, xi[N - 1]));
+        bi = __fma_rn(pr, xi[N - 1], __dmul_rn(pi, xr[N - 1]));
+      } else {
+        br = __fma_rn(-pi, xi[N - 1], __fma_rn(pr, xr[N - 1], br));
+        bi = __fma_rn(pi, xr[N - 1], __fma_rn(pr, xi[N - 1], bi));
+      }
+      return;
+    }
     double pr, pi;
     product(pr, pi);
     if constexpr (C::EXACT) {
