@@ -382,7 +382,8 @@ class Workload:
 
 # ncu --set full summaries of each workload's dominant kernel (profiles/):
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch
-NCU_SUMMARY = {"dense": "r01_ncu_k1_full_summary.csv", "sparse": "r01_ncu_spa_f64_full_summary.csv"}
+NCU_SUMMARY = {"dense": "r01_ncu_k1_full_summary.csv", "sparse": "r01_ncu_spa_f64_full_summary.csv",
+               "haar": "r01_ncu_k3_full_summary.csv"}
 
 
 def ncu_traffic(kind):

@@ -206,13 +206,16 @@ struct DensePlan {
   std::vector<Range> head, tail;
 };
 
-DensePlan plan_dense(int n, int logu, uint64_t start, uint64_t end, int log2_chunk, int ndev) {
+// chunks_log2: automatic chunk size aims at ~2^chunks_log2 chunks per walk
+// (real: 2^22; complex: 2^19, profiles/r01_c128_sweep2.txt)
+DensePlan plan_dense(int n, int logu, uint64_t start, uint64_t end, int log2_chunk, int ndev,
+                     int chunks_log2 = 22) {
   DensePlan pl;
   const uint64_t len = end - start + 1;
   if (logu > 0) {
     int k = log2_chunk;
     if (k <= 0) {
-      k = bit_length(len) - 22;
+      k = bit_length(len) - chunks_log2;
       if (k < logu + 1) k = logu + 1;
     }
     if (k < logu + 1 || k > n - 1 - 5)
@@ -251,6 +254,7 @@ struct Kind {
   int n = 0;
   int streams = 1;            // double-double streams per partial: 1 real, 2 complex
   int logu = 0;               // body length of the register kernel; 0 = walkers only
+  int chunks_log2 = 22;       // automatic chunking target (plan_dense)
   std::vector<double> input;  // uploaded once per device call: cols then x0
   // register kernel over groups [chunk_lo, chunk_lo + 32*groups); returns cudaError_t
   std::function<int(DevCtx&, const double* d_in, uint64_t chunk_lo, uint64_t groups,
@@ -439,6 +443,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   kd.n = n;
   kd.streams = 2;
   kd.logu = (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
+  kd.chunks_log2 = 19;
   const size_t nc = 2 * ncols_of(n);
   kd.input.assign(nc + 2 * n, 0.0);
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
@@ -594,7 +599,8 @@ std::vector<int> device_list(const int* devices, int ndev) {
 void drive(const Kind& kd, uint64_t start, uint64_t end, int log2_chunk,
            const std::vector<int>& devs, dd_t out[2], pk_run_stats* stats) {
   const auto t0 = std::chrono::steady_clock::now();
-  DensePlan pl = plan_dense(kd.n, kd.logu, start, end, log2_chunk, (int)devs.size());
+  DensePlan pl = plan_dense(kd.n, kd.logu, start, end, log2_chunk, (int)devs.size(),
+                            kd.chunks_log2);
   const int nd = pl.num_groups ? (int)devs.size() : 1;
   std::vector<DevResult> res(nd);
   auto work = [&](int i) {

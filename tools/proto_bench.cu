@@ -131,9 +131,13 @@ int main(int argc, char** argv) {
 #define SVAR(NM, NN, UX, MB, KK, GL, R) \
   V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, 128, true>, true>(NM, h##NN, KK, GL, R); }}
   std::vector<V> vs = {
-    VAR("40_k1_fa", 40, 4, 2, 128, true, 18, 23680, 2),
-    VAR("48_k1_fa", 48, 4, 2, 128, true, 20, 4736, 2),
-    VAR("36_k1_fa", 36, 4, 3, 128, true, 14, 0, 3),
+    VAR("40_k15", 40, 4, 2, 128, true, 15, 0, 2),
+    VAR("40_k17", 40, 4, 2, 128, true, 17, 0, 2),
+    VAR("40_k19", 40, 4, 2, 128, true, 19, 0, 2),
+    VAR("40_k21", 40, 4, 2, 128, true, 21, 0, 2),
+    VAR("36_k13", 36, 4, 3, 128, true, 13, 0, 3),
+    VAR("36_k15", 36, 4, 3, 128, true, 15, 0, 3),
+    VAR("36_k17", 36, 4, 3, 128, true, 17, 0, 3),
   };
   for (auto& v : vs) {
     bool sel = argc < 2;

@@ -100,20 +100,19 @@ int main(int argc, char** argv) {
   struct V { const char* name; void (*fn)(); };
 #define CV(NM, NN, UX, MB, FA, KK) V{NM, [] { run<NN, C128Cfg<UX, false, MB, FA>>(NM, h##NN, KK, 3); }}
   std::vector<V> vs = {
-    CV("32_u2_mb2", 32, 2, 2, false, 9),
-    CV("32_u2_mb2_fa", 32, 2, 2, true, 9),
-    CV("32_u3_mb2_fa", 32, 3, 2, true, 9),
-    CV("32_u3_mb1_fa", 32, 3, 1, true, 9),
-    CV("32_u1_mb2_fa", 32, 1, 2, true, 9),
-    CV("32_u2_mb3_fa", 32, 2, 3, true, 9),
-    CV("32_u2_mb2_fa_k12", 32, 2, 2, true, 12),
-    CV("28_u2_mb2", 28, 2, 2, false, 7),
-    CV("28_u2_mb2_fa", 28, 2, 2, true, 7),
-    CV("28_u3_mb2_fa", 28, 3, 2, true, 7),
-    CV("36_u1_mb1", 36, 1, 1, false, 12),
-    CV("36_u1_mb1_fa", 36, 1, 1, true, 12),
-    CV("36_u2_mb1_fa", 36, 2, 1, true, 12),
-    CV("36_u2_mb2_fa", 36, 2, 2, true, 12),
+    CV("32_u2_k9", 32, 2, 2, false, 9),
+    CV("32_u2_k10", 32, 2, 2, false, 10),
+    CV("32_u2_k11", 32, 2, 2, false, 11),
+    CV("32_u2_k12", 32, 2, 2, false, 12),
+    CV("32_u2_k13", 32, 2, 2, false, 13),
+    CV("32_u2_k14", 32, 2, 2, false, 14),
+    CV("32_u2_k16", 32, 2, 2, false, 16),
+    CV("36_u1_k12", 36, 1, 1, false, 12),
+    CV("36_u1_k14", 36, 1, 1, false, 14),
+    CV("36_u1_k16", 36, 1, 1, false, 16),
+    CV("28_u2_k7", 28, 2, 2, false, 7),
+    CV("28_u2_k9", 28, 2, 2, false, 9),
+    CV("28_u2_k11", 28, 2, 2, false, 11),
   };
   for (auto& v : vs) {
     bool sel = argc < 2;
