@@ -159,6 +159,14 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
                          uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
                          double* out_chunks, double out_total[4]);
 
+/* Whole complex walks of `batch` matrices of one order n <= 40 in one launch
+ * (boson-sampling submatrices). cols/x0 back to back in the
+ * pk_dense_c128 layout; out[4*b .. 4*b+3] = (re_hi, re_lo, im_hi, im_lo) of
+ * matrix b's partial over [1, 2^(n-1)-1] (add the g = 0 product and the
+ * sign). Equal bit for bit to pk_dense_c128 with the same chunk exponent. */
+int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, uint32_t flags,
+                        int device, double* out, pk_run_stats* stats);
+
 /* SpaRyser for complex pairs (chunk_sparse_c128, _loops.py:212-235; state of
  * sparse_complex_state, kernels.py:130-143): vals interleaved (re, im) per
  * stored entry, otherwise as pk_sparse_f64. out as pk_dense_c128. The

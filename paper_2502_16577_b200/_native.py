@@ -90,6 +90,8 @@ SIGNATURES = {
                                      _I32, ctypes.c_int, _D, ctypes.POINTER(RunStats)]),
     "pk_spa_f64_source": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
                                          ctypes.c_char_p, ctypes.c_uint64, _U64]),
+    "pk_dense_c128_batch": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
+                                           ctypes.c_int, _D, ctypes.POINTER(RunStats)]),
     "pk_sparse_c128": (ctypes.c_int, [_I64, _I64, _D, ctypes.c_int, _D, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _I32,
                                       ctypes.c_int, _D, ctypes.POINTER(RunStats)]),

@@ -3,10 +3,11 @@
 permkit evaluates decomposition leaves one by one (preprocess.py:495-504),
 and boson-sampling workloads need the permanents of many n ~ 20-30
 submatrices. ``permanent_batch`` groups the matrices by kind and order and
-walks every real group in ONE launch of ``pk_dense_f64_batch`` (one block per
-matrix at a time, each matrix's aligned chunks tree-reduced exactly like a
-single launch). Complex and integer groups fall back to one device call per
-matrix (still on the GPU).
+walks every real group in ONE launch of ``pk_dense_f64_batch`` and every
+complex group of order <= 40 in ONE launch of ``pk_dense_c128_batch`` (one
+block per matrix at a time, each matrix's aligned chunks tree-reduced exactly
+like a single launch). Integer groups and complex orders above 40 take one
+device call per matrix (still on the GPU).
 """
 
 from __future__ import annotations
@@ -19,7 +20,8 @@ import numpy as np
 from . import _native as nat
 from .kernels import (DenseF64Problem, _sign_factor, perm_nw, perm_spa, policy_product,
                       sparse_float_state, total_iterates)
-from .matrix import KIND_REAL, DenseMatrix, SparsePair, coerce_matrix, sparse_to_dense
+from .matrix import (KIND_COMPLEX, KIND_REAL, DenseMatrix, SparsePair, coerce_matrix,
+                     sparse_to_dense)
 from .precision import AccumulatorPolicy, DoubleDouble, as_policy, dd_add
 
 
@@ -54,6 +56,34 @@ def _real_batch(ms: Sequence, policy: AccumulatorPolicy, device: int, exact: boo
     return res
 
 
+def _complex_batch(ms: Sequence, device: int, exact: bool,
+                   stats: Optional[nat.RunStats]) -> List[complex]:
+    from .complex_walk import DenseC128Problem
+    n = ms[0].n
+    probs = [DenseC128Problem(m) for m in ms]
+    b = len(probs)
+    ncol = 2 * (n - 1) * n
+    cols = np.ascontiguousarray(np.concatenate([p.cols[:ncol] for p in probs]) if ncol
+                                else np.zeros(2))
+    x0 = np.ascontiguousarray(np.concatenate([p.x0 for p in probs]))
+    out = np.zeros(4 * b)
+    st = stats if stats is not None else nat.RunStats()
+    rc = nat.load().pk_dense_c128_batch(nat.dptr(cols), nat.dptr(x0), n, b,
+                                        nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out),
+                                        st)
+    nat.check(rc, "pk_dense_c128_batch")
+    res = []
+    sign = _sign_factor(n)
+    for i, p in enumerate(probs):
+        p0 = p.p0()
+        re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+        if n > 1:
+            re = dd_add(re, DoubleDouble(float(out[4 * i]), float(out[4 * i + 1])))
+            im = dd_add(im, DoubleDouble(float(out[4 * i + 2]), float(out[4 * i + 3])))
+        res.append(complex(re.hi * sign, im.hi * sign))
+    return res
+
+
 def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = False,
                     stats: Optional[nat.RunStats] = None) -> list:
     """Permanents of many matrices; results in input order."""
@@ -66,6 +96,13 @@ def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = Fal
     for (kind, n), idx in groups.items():
         if kind == KIND_REAL:
             vals = _real_batch([ms[i] for i in idx], policy, device, exact, stats)
+            for i, v in zip(idx, vals):
+                out[i] = v
+        elif kind == KIND_COMPLEX and n <= 40:
+            if policy is not AccumulatorPolicy.DD:
+                from .errors import PolicyError
+                raise PolicyError("complex matrices support the plain-double policy only")
+            vals = _complex_batch([ms[i] for i in idx], device, exact, stats)
             for i, v in zip(idx, vals):
                 out[i] = v
         else:

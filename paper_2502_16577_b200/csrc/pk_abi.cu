@@ -325,6 +325,22 @@ int dispatch_c128(int n, const pk::C128Launch& a) {
   }
 }
 
+int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_dense_c128_batch<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
 size_t ncols_of(int n) { return (size_t)(n > 1 ? n - 1 : 1) * n; }
 
 Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact,
@@ -1300,6 +1316,80 @@ int pk_spa_c128_source(const double* cols, int n, uint32_t flags, char* buf, uin
       const size_t m = src.size() < cap - 1 ? src.size() : (size_t)cap - 1;
       std::memcpy(buf, src.data(), m);
       buf[m] = '\0';
+    }
+  });
+}
+
+int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, uint32_t flags,
+                        int device, double* out, pk_run_stats* stats) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_n(n);
+    if (batch < 0) fail(PK_ERR_ARG, "negative batch");
+    if (batch == 0) return;
+    if (!x0 || !out || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
+    if (n > pk::kC128NMax) fail(PK_ERR_ARG, "batched complex walks need n <= 40");
+    const size_t ncol = 2 * (size_t)(n > 1 ? n - 1 : 0) * n;
+    DevCtx& c = dev_ctx(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const size_t in_doubles = ncol * batch + 2 * (size_t)n * batch;
+    ensure(c.scratch, c.scratch_cap, in_doubles * 8 + 64);
+    double* d_cols = (double*)c.scratch;
+    double* d_x0 = d_cols + ncol * batch;
+    if (ncol) ck(cudaMemcpyAsync(d_cols, cols, ncol * batch * 8, cudaMemcpyHostToDevice, c.stream), "H2D cols");
+    ck(cudaMemcpyAsync(d_x0, x0, 2 * (size_t)n * batch * 8, cudaMemcpyHostToDevice, c.stream), "H2D x0");
+    ensure(c.chunks, c.chunks_cap, 2 * (size_t)batch);
+    ck(cudaEventRecord(c.e0, c.stream), "event record");
+    int k = 0;
+    if (n >= pk::kC128NMin) {
+      k = pk::batch_log2_chunk(n, pk::c128_logu(n));
+      const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
+      ensure(c.groups, c.groups_cap, 2 * groups * batch);
+      pk::C128BatchLaunch a{};
+      a.d_cols = d_cols;
+      a.d_x0 = d_x0;
+      a.exact = (flags & PK_FLAG_EXACT) != 0;
+      a.batch = batch;
+      a.k = k;
+      a.group_part = c.groups;
+      a.out = c.chunks;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      ck((cudaError_t)dispatch_c128_batch(n, a), "dense_c128 batch launch");
+    } else {
+      const unsigned grid = (unsigned)((batch + pk::kWalkBlock - 1) / pk::kWalkBlock);
+      pk::walk_dense_c128_multi<<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks);
+      ck(cudaGetLastError(), "walk_dense_c128_multi launch");
+    }
+    ck(cudaEventRecord(c.e1, c.stream), "event record");
+    ck(cudaStreamSynchronize(c.stream), "kernel execution");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c.e0, c.e1), "event time");
+    if (k) {
+      // register kernels: (re dd, im dd) per matrix
+      ck(cudaMemcpy(out, c.chunks, (size_t)batch * 2 * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H");
+    } else {
+      // walkers: plain (re, im) per matrix -> (re, 0, im, 0)
+      std::vector<dd_t> w((size_t)batch);
+      ck(cudaMemcpy(w.data(), c.chunks, (size_t)batch * sizeof(dd_t), cudaMemcpyDeviceToHost), "D2H");
+      for (int b = 0; b < batch; ++b) {
+        out[4 * b] = w[b].hi;
+        out[4 * b + 1] = 0.0;
+        out[4 * b + 2] = w[b].lo;
+        out[4 * b + 3] = 0.0;
+      }
+    }
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->kernel_ms = ms;
+      stats->iterates = total_iterates(n) * (uint64_t)batch;
+      stats->log2_chunk = k;
+      stats->devices = 1;
+      stats->launches = 1;
+      stats->chunks = k ? (uint64_t)batch << (n - 1 - k) : 0;
+      stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
   });
 }

@@ -212,18 +212,17 @@ struct C128Steps<N, C, U, U> {
 };
 
 template <int N, class C>
-__device__ __forceinline__ dd_t c128_walk_chunk(const DenseC128Params<N>& p, const double* scols,
-                                                uint64_t c) {
+__device__ __forceinline__ dd_t c128_walk_chunk(const double* x0, int k, uint64_t g_end,
+                                                const double* scols, uint64_t c) {
   constexpr int LOGU = C::LOGU;
   constexpr int U = 1 << LOGU;
   C128Walk<N, C> w;
   w.scols = scols;
-  const int k = p.k;
   const uint64_t base = c << k;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    w.xr[i] = p.x0[2 * i];
-    w.xi[i] = p.x0[2 * i + 1];
+    w.xr[i] = x0[2 * i];
+    w.xi[i] = x0[2 * i + 1];
   }
   // jump-in: x0 + columns of gray(base), ascending (parallel.py:162-188)
   const uint64_t code = base ^ (base >> 1);
@@ -245,7 +244,7 @@ __device__ __forceinline__ dd_t c128_walk_chunk(const DenseC128Params<N>& p, con
     const int jz = (int)(m >> 62);
     C128Steps<N, C, 1, U>::run(w, s_mid, jz);
     const uint64_t g = gb + U;
-    if (m + 1 < nbody || g <= p.g_end) {
+    if (m + 1 < nbody || g <= g_end) {
       const int j = changed_col(g);
       w.update(scols + 2 * j * N, flip_on(g, j) ? 1.0 : -1.0);
       w.fold(false, false);
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(kC128Block, C::MINB)
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
     const uint64_t c = p.chunk_lo + grp * 32 + lane;
-    const dd_t part = c128_walk_chunk<N, C>(p, scols, c);
+    const dd_t part = c128_walk_chunk<N, C>(p.x0, p.k, p.g_end, scols, c);
     if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
     dd_t re{part.hi, 0.0}, im{part.lo, 0.0};
     warp_tree_cdd(re, im);
@@ -289,6 +288,52 @@ __global__ void __launch_bounds__(kC128Block, C::MINB)
 template <int N>
 __host__ __device__ constexpr size_t c128_smem_bytes() {
   return sizeof(double) * 2 * (N - 1) * N;
+}
+
+// ---------------------------------------------------------------------------
+// batched walks (boson-sampling submatrices, decomposition leaves; SURVEY.md
+// §8f-2): one block per matrix at a time, its 2^(N-1-k) aligned chunks walked
+// by the block's warps and reduced exactly like a single launch of the same k
+// (per-component pairwise fold over the group partials).
+
+template <int N>
+struct C128BatchParams {
+  const double* cols;  // [batch][2*(N-1)*N] interleaved
+  const double* x0;    // [batch][2*N]
+  dd_t* group_part;    // [batch][2*groups] scratch
+  dd_t* out;           // [batch][2]: (re, im) partials over [1, 2^(N-1)-1]
+  int batch;
+  int k;
+};
+
+template <int N, class C>
+__global__ void __launch_bounds__(kC128Block, C::MINB)
+    dense_c128_batch(const __grid_constant__ C128BatchParams<N> p) {
+  extern __shared__ __align__(16) double smem[];
+  double* scols = smem;
+  double* sx0 = smem + 2 * (N - 1) * N;
+  const uint64_t total = (1ull << (N - 1)) - 1;
+  const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    __syncthreads();
+    const double* cb = p.cols + (size_t)b * 2 * (N - 1) * N;
+    for (int t = threadIdx.x; t < 2 * (N - 1) * N; t += blockDim.x) scols[t] = cb[t];
+    for (int t = threadIdx.x; t < 2 * N; t += blockDim.x) sx0[t] = p.x0[(size_t)b * 2 * N + t];
+    __syncthreads();
+    dd_t* gp = p.group_part + (size_t)b * 2 * groups;
+    for (int grp = wib; grp < groups; grp += wpb) {
+      const dd_t part = c128_walk_chunk<N, C>(sx0, p.k, total, scols, (uint64_t)grp * 32 + lane);
+      dd_t re{part.hi, 0.0}, im{part.lo, 0.0};
+      warp_tree_cdd(re, im);
+      if (lane == 0) {
+        gp[2 * grp] = re;
+        gp[2 * grp + 1] = im;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) p.out[2 * b + threadIdx.x] = pairwise_fold(gp, 0, groups, 2, threadIdx.x);
+  }
 }
 
 }  // namespace pk

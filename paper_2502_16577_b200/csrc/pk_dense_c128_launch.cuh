@@ -51,6 +51,45 @@ int launch_dense_c128(const C128Launch& a) {
                  : launch_c128_cfg<N, C128Cfg<LOGU, false, MB>>(a, p);
 }
 
+template <int N, class C>
+static int launch_c128_batch_cfg(const C128BatchLaunch& a) {
+  auto kern = dense_c128_batch<N, C>;
+  constexpr size_t smem = c128_smem_bytes<N>() + sizeof(double) * 2 * N;
+  static int occ = -1;
+  if (occ < 0) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kC128Block, smem);
+    if (e != cudaSuccess) return (int)e;
+    occ = o > 0 ? o : 1;
+  }
+  C128BatchParams<N> p;
+  p.cols = a.d_cols;
+  p.x0 = a.d_x0;
+  p.group_part = a.group_part;
+  p.out = a.out;
+  p.batch = a.batch;
+  p.k = a.k;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if ((uint64_t)a.batch < grid) grid = a.batch;
+  kern<<<(unsigned)grid, kC128Block, smem, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_dense_c128_batch(const C128BatchLaunch& a) {
+  constexpr int LOGU = c128_logu(N);
+  constexpr int MB = c128_minb(N);
+  return a.exact ? launch_c128_batch_cfg<N, C128Cfg<LOGU, true, MB>>(a)
+                 : launch_c128_batch_cfg<N, C128Cfg<LOGU, false, MB>>(a);
+}
+
 }  // namespace pk
 
-#define PK_INSTANTIATE_DENSE_C128(N) template int pk::launch_dense_c128<N>(const pk::C128Launch&);
+#define PK_INSTANTIATE_DENSE_C128(N)                                  \
+  template int pk::launch_dense_c128<N>(const pk::C128Launch&); \
+  template int pk::launch_dense_c128_batch<N>(const pk::C128BatchLaunch&);

@@ -89,6 +89,22 @@ struct C128Launch {
 template <int N>
 int launch_dense_c128(const C128Launch& a);
 
+// batched whole complex walks of `batch` matrices of order N (device inputs)
+struct C128BatchLaunch {
+  const double* d_cols;  // [batch][2*(N-1)*N]
+  const double* d_x0;    // [batch][2*N]
+  bool exact;
+  int batch;
+  int k;
+  dd_t* group_part;      // [batch][2 * 2^(N-1-k)/32]
+  dd_t* out;             // [batch][2]
+  cudaStream_t stream;
+  int sms;
+};
+
+template <int N>
+int launch_dense_c128_batch(const C128BatchLaunch& a);
+
 // exact integers (pk_int.cuh): z-space state, |z_i| < 2^zb
 constexpr int kIntNMin = 11;
 constexpr int kIntNMax = 63;

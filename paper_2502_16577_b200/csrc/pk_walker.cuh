@@ -137,6 +137,28 @@ __global__ void __launch_bounds__(kWalkBlock)
   out[r] = dd_t{accr, acci};
 }
 
+// whole complex walks of `batch` small matrices, one thread per matrix
+// (batched API for n < 11): out[r] = (re, im) plain partial
+__global__ void __launch_bounds__(kWalkBlock)
+    walk_dense_c128_multi(const double* __restrict__ cols, const double* __restrict__ x0, int n,
+                          int batch, dd_t* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= batch) return;
+  const double* cr = cols + (size_t)r * 2 * (n - 1) * n;
+  double x[128];
+  for (int i = 0; i < 2 * n; ++i) x[i] = x0[(size_t)r * 2 * n + i];
+  double accr = 0.0, acci = 0.0;
+  const uint64_t end = (1ull << (n - 1)) - 1;
+  for (uint64_t g = 1; g <= end; ++g) {
+    const int j = changed_col(g);
+    const double s = flip_on(g, j) ? 1.0 : -1.0;
+    const double* c = cr + 2 * (size_t)j * n;
+    for (int i = 0; i < n; ++i) c_update_ref(x[2 * i], x[2 * i + 1], s, c[2 * i], c[2 * i + 1]);
+    c_fold_ref(accr, acci, x, n, (g & 1ull) != 0);
+  }
+  out[r] = dd_t{accr, acci};
+}
+
 __global__ void __launch_bounds__(kWalkBlock)
     walk_sparse_c128(const int* __restrict__ cptrs, const int* __restrict__ rids,
                      const double* __restrict__ vals, const double* __restrict__ x0, int n,

@@ -12,3 +12,7 @@ def dense_minb(n: int) -> int:
 
 def batch_log2_chunk(n: int, logu: int) -> int:
     return max(n - 1 - 10, logu + 1)
+
+
+def c128_logu(n: int) -> int:
+    return 2 if n <= 32 else 1

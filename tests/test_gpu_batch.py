@@ -61,3 +61,38 @@ def test_mixed_batch_and_throughput_stats():
     with pytest.raises(pk.PolicyError):  # complex members keep the DD-only rule
         pk.permanent_batch([pk.haar_unitary_block(12, 1)], "kahan")
     assert st.launches == 1 and st.iterates > 0
+
+
+@pytest.mark.parametrize("n", [11, 16, 22, 30])
+@pytest.mark.parametrize("exact", [False, True])
+def test_complex_batch_equals_single_launch_bitwise(n, exact):
+    # one launch for many Haar submatrices (boson sampling) must give each
+    # matrix exactly what pk_dense_c128 gives with the same chunk exponent
+    from paper_2502_16577_b200.complex_walk import DenseC128Problem
+    from paper_2502_16577_b200.csrc_params import c128_logu
+    ms = [pk.haar_unitary_block(n, 40 + s) for s in range(5)]
+    got = pk.permanent_batch(ms, exact=exact)
+    k = batch_log2_chunk(n, c128_logu(n))
+    for m, g in zip(ms, got):
+        prob = DenseC128Problem(m)
+        wr, wi = prob.walk(1, pk.total_iterates(n), exact=exact, log2_chunk=k)
+        p0 = prob.p0()
+        re = dd_add(DoubleDouble(p0.real, 0.0), wr)
+        im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+        s = _sign_factor(n)
+        assert g == complex(re.hi * s, im.hi * s), (n, g)
+
+
+def test_complex_batch_small_orders_and_tolerance(golden):
+    # n < 11: one thread per matrix, the reference loop exactly
+    case = next(c for c in golden["cases"] if c["name"] == "cplx_rand6")
+    m = pk.DenseMatrix.from_array(gio.dense_array(case))
+    serial = case["serial"]["dd"]
+    want = complex(float.fromhex(serial[0]), float.fromhex(serial[1]))
+    got = pk.permanent_batch([m, m, m])
+    assert got[0] == got[2]
+    assert abs(got[0] - want) <= 1e-13 * abs(want)
+    ms = [pk.haar_unitary_block(24, s) for s in range(3)]
+    for g, m in zip(pk.permanent_batch(ms), ms):
+        ref = pk.perm_nw(m)
+        assert abs(g - ref) <= 1e-10 * abs(ref)

@@ -175,6 +175,8 @@ def test_csrc_params_mirror():
     assert "constexpr int dense_logu(int N) { return N <= 50 ? 4 : 3; }" in text
     assert "constexpr int dense_minb(int N) { return N <= 36 ? 3 : 2; }" in text
     assert "(N - 1 - 10) > (logu + 1) ? (N - 1 - 10) : (logu + 1)" in text
+    assert "constexpr int c128_logu(int N) { return N <= 32 ? 2 : 1; }" in text
+    assert cp.c128_logu(32) == 2 and cp.c128_logu(33) == 1
     assert cp.dense_logu(50) == 4 and cp.dense_logu(51) == 3
     assert cp.batch_log2_chunk(20, 4) == 9 and cp.batch_log2_chunk(12, 4) == 5
 
