@@ -383,7 +383,21 @@ class Workload:
 # ncu --set full summaries of each workload's dominant kernel (profiles/):
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch
 NCU_SUMMARY = {"dense": "r01_ncu_k1_full_summary.csv", "sparse": "r01_ncu_spa_f64_full_summary.csv",
-               "haar": "r01_ncu_k3_full_summary.csv"}
+               "haar": "r01_ncu_k3_full_summary.csv", "binary": "r01_ncu_k6_full_summary.csv"}
+
+
+def ncu_metric(kind, metric):
+    """One value from the committed ncu summary of the workload's kernel."""
+    name = NCU_SUMMARY.get(kind)
+    path = os.path.join(ROOT, "profiles", name) if name else None
+    if not path or not os.path.exists(path):
+        return None
+    import csv
+    with open(path) as f:
+        for row in csv.DictReader(f):
+            if row["metric"] == metric:
+                return float(row["value"])
+    return None
 
 
 def ncu_traffic(kind):
@@ -400,6 +414,11 @@ def ncu_traffic(kind):
             if row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 total += float(row["value"]) * scale.get(row["unit"], 1.0)
     return total, "profiles/" + name
+
+
+def _native_sms(dev):
+    import torch
+    return torch.cuda.get_device_properties(dev).multi_processor_count
 
 
 def run_b200(args, dist: Dist):
@@ -491,9 +510,25 @@ def run_b200(args, dist: Dist):
                             "HBM traffic is ~0 (inputs < 32 KB)" % (peaks.get("hbm_gbs"),
                                                                     peaks.get("bf16_tflops"))}
     else:
-        roofline = {"bound": "int-issue", "achieved": None, "peak": None, "unit": "updates/s",
-                    "frac": None, "traffic": None,
-                    "note": "exact integer walk: IMAD/IADD issue bound, no FP64 roofline"}
+        # exact integer walk: no FP64 work; the generated kernel is bound by
+        # instruction issue (IADD/IMAD on the ALU and FMA pipes, 4 warps per
+        # scheduler). achieved = warp instructions per update (ncu
+        # smsp__inst_executed of the same kernel / its updates) x updates/s;
+        # peak = 1 warp instruction per cycle per SM sub-partition.
+        traffic, tsrc = ncu_traffic(wl.kind)
+        inst = ncu_metric(wl.kind, "smsp__inst_executed.sum")
+        upl = ncu_metric(wl.kind, "updates_per_launch")
+        sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+        peak_gi = 4 * _native_sms(dist.local) * sm_mhz * 1e-3
+        ipu = inst / upl * 32 if inst and upl else None  # thread-level instr / update
+        ach = ups / N * ipu / 32 * 1e-9 if ipu else None
+        roofline = {"bound": "issue", "achieved": ach, "peak": peak_gi, "unit": "Gwarp-inst/s",
+                    "frac": ach / peak_gi if ach else None, "traffic": traffic,
+                    "traffic_source": tsrc,
+                    "note": (f"exact integer SpaRyser kernel: {ipu:.1f} instructions per update "
+                             f"(ncu smsp__inst_executed, {tsrc}) x updates/s per GPU vs 4 "
+                             f"schedulers x SMs x SM clock; FP64 roofline does not apply"
+                             if ipu else "exact integer walk: issue bound")}
     cpu = None
     if not args.no_cpu_baseline and N == 1 and wl.kind == "dense":
         cpu = cpu_updates_per_s(n, wl.policy, args.cpu_sample_log2, wl.rows)

@@ -25,6 +25,9 @@ from .parallel import (ChunkPlan, HierarchyPlan, PartialResult, cbl_alignment_re
                        initial_product, matrix_content_hash, merge_partial_files,
                        permanent_chunked, plan_chunks, plan_hierarchy, read_partials_file,
                        reduce_partials, run_range, write_partials_file)
+from .preprocess import (DecompStats, DmResult, Matching, SingularVerdict, d1compress,
+                         d2compress, d34compress, decomp_leaves, decomp_run, decomp_ryser,
+                         dm_decompose, dm_filter, max_matching, min_nnz_row_col)
 from .precision import (AccumulatorPolicy, DoubleDouble, KahanAccumulator, dd_add, dd_mul,
                         kahan_add, reference_permanent, relative_error, two_prod, two_sum)
 

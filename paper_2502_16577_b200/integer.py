@@ -127,16 +127,16 @@ class IntProblem:
         return b
 
 
-def int_walk_total(m, devices=None, stats=None) -> int:
+def int_walk_total(m, devices=None, stats=None, sparse: Optional[bool] = None) -> int:
     """Exact permanent of an integer matrix (perm_nw / perm_spa integer branch,
-    kernels.py:301-306, 339-344)."""
+    kernels.py:301-306, 339-344). sparse: see IntProblem.walk."""
     prob = IntProblem(m)
     n = prob.n
     p0 = prob.p0_y()
     if n == 1:
         from .integer import finalize_int as fin
         return fin(p0, n)
-    words, info = prob.walk(1, (1 << (n - 1)) - 1, devices=devices, stats=stats)
+    words, info = prob.walk(1, (1 << (n - 1)) - 1, devices=devices, stats=stats, sparse=sparse)
     if info.exact_terms:
         part_y = prob.z_to_y(_signed(words, 192), info)
         return finalize_int(p0 + part_y, n)
