@@ -40,6 +40,54 @@ __global__ void mix(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// operand-count probe: 8 chains, distinct second/third operands per chain
+template <int MODE>
+__global__ void ops(double* out, int iters) {
+  double f[8], g[8], h[8];
+  for (int k = 0; k < 8; ++k) {
+    f[k] = threadIdx.x * 1e-3 + k;
+    g[k] = 1.0000001 + k * 1e-9 + threadIdx.x * 1e-12;
+    h[k] = 1e-9 * (k + 1);
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (MODE == 0) f[k] = fma(f[k], g[k], h[k]);          // 3 distinct operands
+        else if (MODE == 1) f[k] = f[k] * g[k];               // DMUL, 2 operands
+        else if (MODE == 2) f[k] = f[k] + g[k];               // DADD, 2 operands
+        else f[k] = fma(f[k], g[0], h[0]);                    // shared operands (reuse)
+      }
+  }
+  double s = 0;
+  for (int k = 0; k < 8; ++k) s += f[k];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int MODE>
+void run_ops(const char* name, int sms, int iters) {
+  double* o;
+  CK(cudaMalloc(&o, 8));
+  const int blocks = sms * 8, threads = 256;
+  ops<MODE><<<blocks, threads>>>(o, 10);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    ops<MODE><<<blocks, threads>>>(o, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double inst = 8.0 * 16 * (double)iters * blocks * threads;
+  printf("%-22s ms=%8.3f  %.3f T FP64-instr/s (lane ops)\n", name, best, inst / (best * 1e-3) * 1e-12);
+  cudaFree(o);
+}
+
 template <int NF, int NM, int RF, int RM>
 void run(const char* name, int sms, int blocks_per_sm, int threads, int iters) {
   double* o;
@@ -80,5 +128,9 @@ int main() {
   run<8, 4, 16, 4>("mix_16f:4m", sms, 8, 256, it);
   run<8, 4, 16, 8>("mix_16f:8m", sms, 8, 256, it);
   run<8, 4, 8, 16>("mix_8f:16m", sms, 8, 256, it);
+  run_ops<0>("dfma_3_distinct", sms, it);
+  run_ops<1>("dmul_2_distinct", sms, it);
+  run_ops<2>("dadd_2_distinct", sms, it);
+  run_ops<3>("dfma_shared_ops", sms, it);
   return 0;
 }
