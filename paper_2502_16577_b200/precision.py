@@ -56,7 +56,12 @@ _CODES = {AccumulatorPolicy.DD: 0, AccumulatorPolicy.KAHAN: 1, AccumulatorPolicy
 
 
 def as_policy(p: "AccumulatorPolicy | str") -> AccumulatorPolicy:
-    return p if isinstance(p, AccumulatorPolicy) else AccumulatorPolicy.parse(p)
+    """This package's policy, its name, or permkit's own enum member (duck
+    typed on its string .value) -> AccumulatorPolicy."""
+    if isinstance(p, AccumulatorPolicy):
+        return p
+    v = getattr(p, "value", None)
+    return AccumulatorPolicy.parse(v if isinstance(v, str) else p)
 
 
 class DoubleDouble(NamedTuple):

@@ -190,8 +190,10 @@ def test_generated_spa_source_compiles_for_sm100a(tmp_path):
     src = spa_source(m)
     assert "spa_int" in src and "switch (j)" in src
     nnz_col0 = sum(1 for i in range(24) if m.entry(i, 0))
-    body = src.split("const int smid")[1].split("{", 1)[1].split("int g0")[0]
-    assert body.count("z") == nnz_col0
+    # float-group kernel (default): step 1 adds literal 2*a_i0 to z_i, nonzeros only
+    body = src.split("const float smid")[1].split("{", 1)[1].split("const float f0")[0]
+    assert body.count(".0f;") == nnz_col0
+    assert "addsub128" in src and "__umul64hi" in src
     f = tmp_path / "spa.cu"
     f.write_text(src)
     r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-gencode",
