@@ -42,6 +42,12 @@ extern "C" {
 #define PK_ERR_IMPOSSIBLE 4 /* ImpossibleError: n > 63 (matrix.py:35-42)      */
 #define PK_ERR_CUDA 5       /* device missing or a CUDA call failed           */
 #define PK_ERR_OVERFLOW 6   /* exact integer path cannot represent the values */
+#define PK_ERR_TIMEOUT 7    /* DecompTimeout: task or wall-clock budget spent */
+
+/* matrix kinds (matrix.py:25-28) */
+#define PK_KIND_REAL 0
+#define PK_KIND_COMPLEX 1
+#define PK_KIND_INT 2
 
 /* accumulator policies, same codes as _loops.py:27-30 */
 #define PK_POLICY_DD 0
@@ -208,6 +214,49 @@ int pk_int_spa_source(const int64_t* a, int n, char* buf, uint64_t cap, uint64_t
 /* one exact partial per range (walkers, one device thread each): 3 words each */
 int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_t* ends,
                   int nranges, int device, uint64_t* out_z, pk_int_info* info);
+
+/* ------------------------------------------------ decomposition worklist
+ * The task tree of permkit's decomp_run (preprocess.py:420-507): LIFO
+ * worklist of d1 / d2 / d34 compressions (:289-364) on the sparsest row or
+ * column, until every row and column has more than `threshold` nonzeros.
+ * Host code (no device work): the caller evaluates the kernel leaves (e.g.
+ * in batched launches) and combines contributions in task-id order.
+ * a: dense row-major n x n matrix, zeros = absent entries; doubles (real),
+ * interleaved (re, im) doubles (complex) or int64 (integer). Integers are
+ * exact in 128 bits; beyond that PK_ERR_OVERFLOW. Budgets: PK_ERR_TIMEOUT.
+ * On success *handle owns the outputs: fetch them, then free the handle. */
+typedef struct pk_decomp_stats {
+  uint64_t tasks_created;
+  uint64_t d1_applied;
+  uint64_t d2_applied;
+  uint64_t d34_applied;
+  uint64_t trivial_leaves;
+  uint64_t kernel_leaves;
+  uint64_t dense_kernel_leaves;
+  int64_t max_depth;
+  double elapsed_s;
+} pk_decomp_stats;
+
+typedef struct pk_decomp_result {
+  pk_decomp_stats stats;
+  int64_t trivial;      /* n = 1 contributions (task id, multiplier * a_00) */
+  int64_t leaves;       /* kernel leaves (task id, order, multiplier, matrix) */
+  int64_t leaf_values;  /* total scalars of the concatenated leaf matrices */
+} pk_decomp_result;
+
+/* acc = dd_add(acc, (vals[k], 0)) for k in order from (0, 0) (the robust
+ * double-double add of precision.py:84-96): permkit's leaf combination */
+int pk_dd_accumulate(const double* vals, int64_t count, double out[2]);
+
+int pk_decomp_tree(int kind, int n, const void* a, int threshold, uint64_t task_limit,
+                   double time_limit, double dense_density, void** handle,
+                   pk_decomp_result* res);
+/* scalars: 1 double (real), 2 doubles (complex), 2 int64 words (integer,
+ * little-endian two's complement 128-bit); any pointer may be NULL */
+int pk_decomp_fetch(void* handle, int64_t* triv_id, void* triv_val, int64_t* leaf_id,
+                    int32_t* leaf_n, void* leaf_mult, void* leaf_vals);
+void pk_decomp_free(void* handle);
+const char* pk_decomp_last_error(void);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,23 @@ class RunStats(ctypes.Structure):
 _lib = None
 _lock = threading.Lock()
 
+
+class DecompStats_(ctypes.Structure):
+    _fields_ = [("tasks_created", ctypes.c_uint64), ("d1_applied", ctypes.c_uint64),
+                ("d2_applied", ctypes.c_uint64), ("d34_applied", ctypes.c_uint64),
+                ("trivial_leaves", ctypes.c_uint64), ("kernel_leaves", ctypes.c_uint64),
+                ("dense_kernel_leaves", ctypes.c_uint64), ("max_depth", ctypes.c_int64),
+                ("elapsed_s", ctypes.c_double)]
+
+
+class DecompResult(ctypes.Structure):
+    _fields_ = [("stats", DecompStats_), ("trivial", ctypes.c_int64), ("leaves", ctypes.c_int64),
+                ("leaf_values", ctypes.c_int64)]
+
+
+PK_KIND_REAL, PK_KIND_COMPLEX, PK_KIND_INT = 0, 1, 2
+PK_ERR_TIMEOUT = 7
+
 _D = ctypes.POINTER(ctypes.c_double)
 _U64 = ctypes.POINTER(ctypes.c_uint64)
 _I32 = ctypes.POINTER(ctypes.c_int32)
@@ -97,6 +114,15 @@ SIGNATURES = {
                                       ctypes.c_int, _D, ctypes.POINTER(RunStats)]),
     "pk_spa_c128_source": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_uint32, ctypes.c_char_p,
                                           ctypes.c_uint64, _U64]),
+    "pk_dd_accumulate": (ctypes.c_int, [_D, ctypes.c_int64, _D]),
+    "pk_decomp_tree": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                      ctypes.POINTER(ctypes.c_void_p),
+                                      ctypes.POINTER(DecompResult)]),
+    "pk_decomp_fetch": (ctypes.c_int, [ctypes.c_void_p, _I64, ctypes.c_void_p, _I64, _I32,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
+    "pk_decomp_free": (None, [ctypes.c_void_p]),
+    "pk_decomp_last_error": (ctypes.c_char_p, []),
     "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                               ctypes.c_int, _I32, ctypes.c_int, _U64, ctypes.c_void_p,
                               ctypes.POINTER(RunStats)]),

@@ -25,30 +25,43 @@ from .matrix import (KIND_COMPLEX, KIND_REAL, DenseMatrix, SparsePair, coerce_ma
 from .precision import AccumulatorPolicy, DoubleDouble, as_policy, dd_add
 
 
-def _real_batch(ms: Sequence, policy: AccumulatorPolicy, device: int, exact: bool,
-                stats: Optional[nat.RunStats]) -> List[float]:
+def dense_states(A: np.ndarray):
+    """Vectorised dense_float_state / dense_complex_state of a stack of
+    matrices A[b, n, n] (kernels.py:75-101): columns cols[b, j, i] = a_ij for
+    j < n-1 and the seed x0 = a[:, n-1] - rowsum / 2 with the row sums taken
+    left to right (np.add.accumulate is sequential: the reference's rounding
+    order, matrix.py:333-355)."""
+    b, n, _ = A.shape
+    sums = np.add.accumulate(A, axis=2)[:, :, n - 1]
+    x0 = np.ascontiguousarray(A[:, :, n - 1] - sums / 2.0)
+    cols = np.ascontiguousarray(np.transpose(A[:, :, : n - 1], (0, 2, 1)))
+    return cols, x0
+
+
+def _stack(ms: Sequence, dtype) -> np.ndarray:
     n = ms[0].n
-    probs = []
+    rows = []
     for m in ms:
-        if isinstance(m, SparsePair):
-            pr = DenseF64Problem(sparse_to_dense(m))
-            pr.x0 = np.ascontiguousarray(sparse_float_state(m)[3], dtype=np.float64)
-        else:
-            pr = DenseF64Problem(m)
-        probs.append(pr)
-    b = len(probs)
-    ncol = (n - 1) * n
-    cols = np.ascontiguousarray(np.concatenate([p.cols[:ncol] for p in probs]) if ncol
-                                else np.zeros(1))
-    x0 = np.ascontiguousarray(np.concatenate([p.x0 for p in probs]))
+        d = sparse_to_dense(m) if isinstance(m, SparsePair) else m
+        rows.append(np.array(d.data, dtype=dtype).reshape(n, n))
+    return np.stack(rows)
+
+
+def real_batch_arrays(A: np.ndarray, policy: AccumulatorPolicy, device: int = 0,
+                      exact: bool = False, stats: Optional[nat.RunStats] = None) -> List[float]:
+    """Permanents of the real matrices A[b, n, n] in one pk_dense_f64_batch launch."""
+    b, n, _ = A.shape
+    cols, x0 = dense_states(np.asarray(A, dtype=np.float64))
+    cflat = np.ascontiguousarray(cols.reshape(-1)) if n > 1 else np.zeros(1)
+    xflat = np.ascontiguousarray(x0.reshape(-1))
     out = np.zeros(2 * b)
     st = stats if stats is not None else nat.RunStats()
-    rc = nat.load().pk_dense_f64_batch(nat.dptr(cols), nat.dptr(x0), n, b, policy.code,
+    rc = nat.load().pk_dense_f64_batch(nat.dptr(cflat), nat.dptr(xflat), n, b, policy.code,
                                        nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out), st)
     nat.check(rc, "pk_dense_f64_batch")
     res = []
-    for i, p in enumerate(probs):
-        p0 = policy_product(p.x0, policy)
+    for i in range(b):
+        p0 = policy_product(x0[i], policy)
         acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
         if n > 1:
             acc = dd_add(acc, DoubleDouble(float(out[2 * i]), float(out[2 * i + 1])))
@@ -56,32 +69,42 @@ def _real_batch(ms: Sequence, policy: AccumulatorPolicy, device: int, exact: boo
     return res
 
 
-def _complex_batch(ms: Sequence, device: int, exact: bool,
-                   stats: Optional[nat.RunStats]) -> List[complex]:
-    from .complex_walk import DenseC128Problem
-    n = ms[0].n
-    probs = [DenseC128Problem(m) for m in ms]
-    b = len(probs)
-    ncol = 2 * (n - 1) * n
-    cols = np.ascontiguousarray(np.concatenate([p.cols[:ncol] for p in probs]) if ncol
-                                else np.zeros(2))
-    x0 = np.ascontiguousarray(np.concatenate([p.x0 for p in probs]))
+def complex_batch_arrays(A: np.ndarray, device: int = 0, exact: bool = False,
+                         stats: Optional[nat.RunStats] = None) -> List[complex]:
+    """Permanents of the complex matrices A[b, n, n] (n <= 40) in one
+    pk_dense_c128_batch launch."""
+    b, n, _ = A.shape
+    cols, x0 = dense_states(np.asarray(A, dtype=np.complex128))
+    cflat = np.ascontiguousarray(cols.reshape(-1).view(np.float64)) if n > 1 else np.zeros(2)
+    xflat = np.ascontiguousarray(x0.reshape(-1).view(np.float64))
     out = np.zeros(4 * b)
     st = stats if stats is not None else nat.RunStats()
-    rc = nat.load().pk_dense_c128_batch(nat.dptr(cols), nat.dptr(x0), n, b,
+    rc = nat.load().pk_dense_c128_batch(nat.dptr(cflat), nat.dptr(xflat), n, b,
                                         nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out),
                                         st)
     nat.check(rc, "pk_dense_c128_batch")
     res = []
     sign = _sign_factor(n)
-    for i, p in enumerate(probs):
-        p0 = p.p0()
-        re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+    for i in range(b):
+        p = complex(1.0)
+        for v in x0[i]:
+            p = p * complex(v)
+        re, im = DoubleDouble(p.real, 0.0), DoubleDouble(p.imag, 0.0)
         if n > 1:
             re = dd_add(re, DoubleDouble(float(out[4 * i]), float(out[4 * i + 1])))
             im = dd_add(im, DoubleDouble(float(out[4 * i + 2]), float(out[4 * i + 3])))
         res.append(complex(re.hi * sign, im.hi * sign))
     return res
+
+
+def _real_batch(ms: Sequence, policy: AccumulatorPolicy, device: int, exact: bool,
+                stats: Optional[nat.RunStats]) -> List[float]:
+    return real_batch_arrays(_stack(ms, np.float64), policy, device, exact, stats)
+
+
+def _complex_batch(ms: Sequence, device: int, exact: bool,
+                   stats: Optional[nat.RunStats]) -> List[complex]:
+    return complex_batch_arrays(_stack(ms, np.complex128), device, exact, stats)
 
 
 def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = False,

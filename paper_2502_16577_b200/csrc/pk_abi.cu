@@ -1394,4 +1394,16 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
   });
 }
 
+// acc = dd_add(acc, (v_k, 0)) over k in order, from acc = (0, 0): the
+// reference's leaf combination (preprocess.py:398-417) for one component
+int pk_dd_accumulate(const double* vals, int64_t count, double out[2]) {
+  return guarded([&] {
+    if ((!vals && count > 0) || !out || count < 0) fail(PK_ERR_ARG, "bad arguments");
+    dd_t acc{0.0, 0.0};
+    for (int64_t k = 0; k < count; ++k) acc = h_dd_add(acc, dd_t{vals[k], 0.0});
+    out[0] = acc.hi;
+    out[1] = acc.lo;
+  });
+}
+
 }  // extern "C"

@@ -464,18 +464,24 @@ def _combine_contributions(contribs: List[Tuple[int, Scalar]], kind: str) -> Sca
     contribs.sort(key=lambda t: t[0])
     if kind == KIND_INT:
         return sum(v for _, v in contribs)
+    import numpy as np
     if kind == KIND_COMPLEX:
-        re = DoubleDouble(0.0, 0.0)
-        im = DoubleDouble(0.0, 0.0)
-        for _, v in contribs:
-            c = complex(v)
-            re = dd_add(re, DoubleDouble.from_float(c.real))
-            im = dd_add(im, DoubleDouble.from_float(c.imag))
-        return complex(re.hi, im.hi)
-    acc = DoubleDouble(0.0, 0.0)
-    for _, v in contribs:
-        acc = dd_add(acc, DoubleDouble.from_float(float(v)))
-    return acc.hi
+        vals = np.array([complex(v) for _, v in contribs], dtype=np.complex128)
+        return complex(_dd_sum(np.ascontiguousarray(vals.real)),
+                       _dd_sum(np.ascontiguousarray(vals.imag)))
+    return _dd_sum(np.array([float(v) for _, v in contribs], dtype=np.float64))
+
+
+def _dd_sum(vals) -> float:
+    """hi of the in-order double-double sum of vals (one C call; the same
+    dd_add sequence as the reference's loop)."""
+    from . import _native as nat
+    import numpy as np
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    out = np.zeros(2)
+    nat.check(nat.load().pk_dd_accumulate(nat.dptr(vals) if len(vals) else None, len(vals),
+                                          nat.dptr(out)), "pk_dd_accumulate")
+    return float(out[0])
 
 
 class _LeafQueue:
@@ -580,24 +586,161 @@ def _decompose(s: SparsePair, stats: DecompStats, contribs: List[Tuple[int, Scal
     stats.elapsed = time.monotonic() - started
 
 
+def _native_tree(s: SparsePair, task_limit: int, time_limit: float, min_nnz_threshold: int,
+                 dense_leaf_density: float):
+    """The task tree from the native worklist (csrc/pk_decomp.cu): (trivial
+    contributions, leaves grouped by order {n: (task ids, multipliers,
+    matrices[b, n, n])}, stats); None when the integers outgrow 128 bits
+    (the Python worklist then takes over with arbitrary precision)."""
+    import ctypes
+
+    import numpy as np
+
+    from . import _native as nat
+    from .matrix import sparse_to_dense
+    n, kind = s.n, s.kind
+    dense = sparse_to_dense(s)
+    if kind == KIND_INT:
+        code, dt, width = nat.PK_KIND_INT, np.int64, 2
+        a = np.array([int(v) for v in dense.data], dtype=object)
+        if any(abs(int(v)) >= (1 << 63) for v in a):
+            return None
+        a = np.ascontiguousarray(a.astype(np.int64))
+    elif kind == KIND_COMPLEX:
+        code, dt, width = nat.PK_KIND_COMPLEX, np.float64, 2
+        a = np.ascontiguousarray(np.array(dense.data, dtype=np.complex128).view(np.float64))
+    else:
+        code, dt, width = nat.PK_KIND_REAL, np.float64, 1
+        a = np.ascontiguousarray(np.array(dense.data, dtype=np.float64))
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    res = nat.DecompResult()
+    rc = lib.pk_decomp_tree(code, n, a.ctypes.data_as(ctypes.c_void_p), min_nnz_threshold,
+                            task_limit, time_limit, dense_leaf_density, ctypes.byref(h),
+                            ctypes.byref(res))
+    if rc == nat.PK_ERR_OVERFLOW:
+        return None
+    if rc == nat.PK_ERR_TIMEOUT:
+        raise DecompTimeout(lib.pk_decomp_last_error().decode(),
+                            tasks_done=int(res.stats.tasks_created))
+    if rc != nat.PK_OK:
+        raise StructureError(lib.pk_decomp_last_error().decode())
+    try:
+        nt, nl, nv = int(res.trivial), int(res.leaves), int(res.leaf_values)
+        t_id = np.zeros(max(nt, 1), dtype=np.int64)
+        t_val = np.zeros(max(nt, 1) * width, dtype=dt)
+        l_id = np.zeros(max(nl, 1), dtype=np.int64)
+        l_n = np.zeros(max(nl, 1), dtype=np.int32)
+        l_mult = np.zeros(max(nl, 1) * width, dtype=dt)
+        l_vals = np.zeros(max(nv, 1) * width, dtype=dt)
+        vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+        lib.pk_decomp_fetch(h, nat.i64ptr(t_id), vp(t_val), nat.i64ptr(l_id), nat.i32ptr(l_n),
+                            vp(l_mult), vp(l_vals))
+    finally:
+        lib.pk_decomp_free(h)
+
+    def scalar(arr, k):
+        if kind == KIND_INT:
+            lo, hi = int(arr[2 * k]) & ((1 << 64) - 1), int(arr[2 * k + 1])
+            return (hi << 64) | lo
+        if kind == KIND_COMPLEX:
+            return complex(float(arr[2 * k]), float(arr[2 * k + 1]))
+        return float(arr[k])
+
+    trivial = [(int(t_id[k]), scalar(t_val, k)) for k in range(nt)]
+    groups: Dict[int, Tuple[List[int], List[Scalar], List[int]]] = defaultdict(
+        lambda: ([], [], []))
+    off = 0
+    for k in range(nl):
+        m = int(l_n[k])
+        g = groups[m]
+        g[0].append(int(l_id[k]))
+        g[1].append(scalar(l_mult, k))
+        g[2].append(off)
+        off += m * m
+    leaves = {}
+    for m, (ids, mults, offs) in groups.items():
+        if kind == KIND_INT:
+            vals = l_vals.reshape(-1, 2)
+            mats = [[[scalar(l_vals, o + i * m + j) for j in range(m)] for i in range(m)]
+                    for o in offs]
+        elif kind == KIND_COMPLEX:
+            c = l_vals.view(np.complex128)
+            mats = np.stack([c[o:o + m * m].reshape(m, m) for o in offs])
+        else:
+            mats = np.stack([l_vals[o:o + m * m].reshape(m, m) for o in offs])
+        leaves[m] = (ids, mults, mats)
+    st = res.stats
+    stats = DecompStats(tasks_created=int(st.tasks_created), d1_applied=int(st.d1_applied),
+                        d2_applied=int(st.d2_applied), d34_applied=int(st.d34_applied),
+                        trivial_leaves=int(st.trivial_leaves), kernel_leaves=int(st.kernel_leaves),
+                        dense_kernel_leaves=int(st.dense_kernel_leaves),
+                        max_depth=int(st.max_depth))
+    for m, (ids, _, _) in leaves.items():
+        stats.leaf_sizes.extend([m] * len(ids))
+    return trivial, leaves, stats
+
+
+def _evaluate_native_leaves(leaves, kind, policy, device, stats, contribs) -> None:
+    """Batched device evaluation of the native tree's leaves (one launch per
+    order for real / complex; exact integer kernels per leaf)."""
+    from .batch import complex_batch_arrays, real_batch_arrays
+    from .integer import int_walk_total
+    from .matrix import DenseMatrix
+    for m, (ids, mults, mats) in sorted(leaves.items()):
+        if kind == KIND_INT:
+            for tid, mult, rows in zip(ids, mults, mats):
+                v = int_walk_total(DenseMatrix.from_rows(rows, kind=KIND_INT), [device],
+                                   sparse=False)
+                contribs.append((tid, mult * v))
+                stats.leaf_launches += 1
+            continue
+        for lo in range(0, len(ids), LEAF_BATCH):
+            chunk = mats[lo:lo + LEAF_BATCH]
+            if kind == KIND_COMPLEX and m <= 40:
+                if policy is not AccumulatorPolicy.DD:
+                    from .errors import PolicyError
+                    raise PolicyError("complex matrices support the plain-double policy only")
+                vals = complex_batch_arrays(chunk, device)
+            elif kind == KIND_COMPLEX:
+                from .batch import permanent_batch
+                vals = permanent_batch([DenseMatrix.from_array(x) for x in chunk], policy,
+                                       device=device)
+            else:
+                vals = real_batch_arrays(chunk, policy, device)
+            stats.leaf_launches += 1
+            for tid, mult, v in zip(ids[lo:lo + LEAF_BATCH], mults[lo:lo + LEAF_BATCH], vals):
+                contribs.append((tid, mult * v))
+
+
 def decomp_run(s: SparsePair, policy: "AccumulatorPolicy | str" = AccumulatorPolicy.DD,
                task_limit: int = DEFAULT_TASK_LIMIT, time_limit: float = DEFAULT_TIME_LIMIT,
                min_nnz_threshold: int = 4, dense_leaf_density: float = DENSE_LEAF_DENSITY,
-               *, device: int = 0) -> Tuple[Scalar, DecompStats]:
+               *, device: int = 0, native: bool = True) -> Tuple[Scalar, DecompStats]:
     """Worklist compression driver; returns (permanent, statistics)
     (preprocess.py:420-507). Tasks are processed LIFO; exceeding the task or
-    wall-clock budget raises DecompTimeout with progress attached. Kernel
-    leaves are evaluated in batches on `device` (module docstring); the
-    leaf's density only feeds the statistics, because every leaf goes to the
-    dense batched kernels (x + 0 == x: the sparse walk's arithmetic)."""
+    wall-clock budget raises DecompTimeout with progress attached.
+
+    The task tree is walked by the native worklist (csrc/pk_decomp.cu; the
+    Python one below when native=False or integers outgrow 128 bits), and
+    kernel leaves are evaluated in batched launches on `device` (module
+    docstring); every leaf goes to the dense batched kernels (x + 0 == x: the
+    sparse walk's arithmetic), its density only feeds the statistics."""
     policy = as_policy(policy)
-    stats = DecompStats()
     started = time.monotonic()
     contribs: List[Tuple[int, Scalar]] = []
-    leaves = _LeafQueue(s.kind, policy, device, stats)
-    _decompose(s, stats, contribs, lambda t, m, a: leaves.add(t, m, a, contribs), task_limit,
-               time_limit, min_nnz_threshold, dense_leaf_density)
-    leaves.flush(contribs)
+    tree = _native_tree(s, task_limit, time_limit, min_nnz_threshold,
+                        dense_leaf_density) if native else None
+    if tree is not None:
+        trivial, leaves, stats = tree
+        contribs.extend(trivial)
+        _evaluate_native_leaves(leaves, s.kind, policy, device, stats, contribs)
+    else:
+        stats = DecompStats()
+        leaves_q = _LeafQueue(s.kind, policy, device, stats)
+        _decompose(s, stats, contribs, lambda t, m, a: leaves_q.add(t, m, a, contribs),
+                   task_limit, time_limit, min_nnz_threshold, dense_leaf_density)
+        leaves_q.flush(contribs)
     stats.elapsed = time.monotonic() - started
     return _combine_contributions(contribs, s.kind), stats
 

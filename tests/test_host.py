@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "permkit_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pk_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(pk_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():

@@ -173,6 +173,10 @@ def test_decomp_run_matches_reference_value(name):
     gold = c["decomp"]
     got, st = pp.decomp_run(s, gold["policy"])
     want = dec(gold["value"], kind)
+    # the native and the Python worklists build the same tree and the leaves
+    # go through the same batched kernels: identical results
+    got_py, st_py = pp.decomp_run(s, gold["policy"], native=False)
+    assert got == got_py and st.tasks_created == st_py.tasks_created
     if kind == "integer":
         assert got == want
     else:
@@ -198,3 +202,62 @@ def test_decomp_leaf_values_match_reference():
                 assert v == w
             else:
                 assert abs(v - w) <= 1e-10 * abs(w) + 1e-300, (name, v, w)
+
+
+def native_leaves(s):
+    """The native worklist's tree in the shape of decomp_leaves' output."""
+    trivial, leaves, st = pp._native_tree(s, pp.DEFAULT_TASK_LIMIT, 1e9, 4, pp.DENSE_LEAF_DENSITY)
+    out = []
+    for n, (ids, mults, mats) in leaves.items():
+        for tid, mult, mat in zip(ids, mults, mats):
+            rows = [[mat[i][j] for j in range(n)] for i in range(n)]
+            trip = [(i, j, rows[i][j]) for i in range(n) for j in range(n) if rows[i][j] != 0]
+            out.append((tid, mult, pk.sparse_from_triplets(n, trip, s.kind)))
+    return out, trivial, st
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_native_tree_equals_python_tree_and_reference(name):
+    c = case(name)
+    s = pair(c)
+    kind = c["kind"]
+    nat_leaves, nat_triv, nst = native_leaves(s)
+    py_leaves, py_triv, pst = pp.decomp_leaves(s)
+    for k in ("tasks_created", "d1_applied", "d2_applied", "d34_applied", "trivial_leaves",
+              "kernel_leaves", "max_depth"):
+        assert getattr(nst, k) == getattr(pst, k) == c["decomp"]["stats"][k], k
+    assert sorted(nat_triv, key=lambda t: t[0]) == sorted(py_triv, key=lambda t: t[0])
+    py = {tid: (mult, m) for tid, mult, m in py_leaves}
+    assert len(nat_leaves) == len(py_leaves)
+    for tid, mult, m in nat_leaves:
+        pm, pmat = py[tid]
+        assert mult == pm
+        got = m.crs.triplets()
+        want = pmat.crs.triplets()
+        assert [(i, j) for i, j, _ in got] == [(i, j) for i, j, _ in want]
+        for (_, _, v), (_, _, w) in zip(got, want):
+            if kind == "real64":
+                assert float(v).hex() == float(w).hex()
+            else:
+                assert v == w
+    if not nat_leaves:
+        got = pp._combine_contributions(list(nat_triv), kind)
+        want = dec(c["decomp"]["value"], kind)
+        assert got == want
+
+
+def test_dense_states_match_scalar_state_builders():
+    from paper_2502_16577_b200.batch import dense_states
+    from paper_2502_16577_b200.kernels import dense_complex_state, dense_float_state
+    rng = np.random.default_rng(5)
+    for n in (2, 7, 20):
+        A = rng.uniform(-1, 1, size=(4, n, n)) * (rng.uniform(size=(4, n, n)) < 0.6)
+        cols, x0 = dense_states(A)
+        for b in range(4):
+            c1, x1 = dense_float_state(pk.DenseMatrix.from_array(A[b]))
+            assert np.array_equal(cols[b], c1) and x0[b].tobytes() == x1.tobytes()
+        C = A + 1j * rng.uniform(-1, 1, size=(4, n, n))
+        cols, x0 = dense_states(C)
+        for b in range(4):
+            c1, x1 = dense_complex_state(pk.DenseMatrix.from_array(C[b]))
+            assert np.array_equal(cols[b], c1) and x0[b].tobytes() == x1.tobytes()
