@@ -208,6 +208,14 @@ typedef struct pk_int_info {
 int pk_int(const int64_t* a, int n, uint64_t start, uint64_t end, uint32_t flags, int log2_chunk,
            const int* devices, int ndev, uint64_t out_z[3], pk_int_info* info,
            pk_run_stats* stats);
+/* Whole exact walks of `batch` integer matrices of one order in one launch
+ * (decomposition leaves): a holds the matrices back to back (n*n int64
+ * each); out_z[3*b..3*b+2] = matrix b's z-space partial over
+ * [1, 2^(n-1)-1] (add its g = 0 term and rescale as pk_int's), info[b] its
+ * z-space facts. Every matrix must have exact_terms (else PK_ERR_OVERFLOW;
+ * the caller then walks it alone, which has the modular route). */
+int pk_int_batch(const int64_t* a, int n, int batch, int device, uint64_t* out_z,
+                 pk_int_info* info, pk_run_stats* stats);
 /* the CUDA source of the generated SpaRyser kernel for `a` (n >= 11): copies
  * at most cap-1 bytes + NUL into buf, *len = full length */
 int pk_int_spa_source(const int64_t* a, int n, char* buf, uint64_t cap, uint64_t* len);

@@ -126,6 +126,8 @@ SIGNATURES = {
     "pk_int": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                               ctypes.c_int, _I32, ctypes.c_int, _U64, ctypes.c_void_p,
                               ctypes.POINTER(RunStats)]),
+    "pk_int_batch": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _U64,
+                                    ctypes.c_void_p, ctypes.POINTER(RunStats)]),
     "pk_int_spa_source": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_char_p, ctypes.c_uint64,
                                          _U64]),
     "pk_int_ranges": (ctypes.c_int, [_I64, ctypes.c_int, _U64, _U64, ctypes.c_int, ctypes.c_int,

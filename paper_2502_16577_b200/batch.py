@@ -4,10 +4,11 @@ permkit evaluates decomposition leaves one by one (preprocess.py:495-504),
 and boson-sampling workloads need the permanents of many n ~ 20-30
 submatrices. ``permanent_batch`` groups the matrices by kind and order and
 walks every real group in ONE launch of ``pk_dense_f64_batch`` and every
-complex group of order <= 40 in ONE launch of ``pk_dense_c128_batch`` (one
-block per matrix at a time, each matrix's aligned chunks tree-reduced exactly
-like a single launch). Integer groups and complex orders above 40 take one
-device call per matrix (still on the GPU).
+complex group of order <= 40 in ONE launch of ``pk_dense_c128_batch`` and
+every integer group in ONE launch of ``pk_int_batch`` (one block per matrix
+at a time, each matrix's aligned chunks reduced exactly like a single
+launch). Complex orders above 40 take one device call per matrix (still on
+the GPU).
 """
 
 from __future__ import annotations
@@ -20,7 +21,7 @@ import numpy as np
 from . import _native as nat
 from .kernels import (DenseF64Problem, _sign_factor, perm_nw, perm_spa, policy_product,
                       sparse_float_state, total_iterates)
-from .matrix import (KIND_COMPLEX, KIND_REAL, DenseMatrix, SparsePair, coerce_matrix,
+from .matrix import (KIND_COMPLEX, KIND_INT, KIND_REAL, DenseMatrix, SparsePair, coerce_matrix,
                      sparse_to_dense)
 from .precision import AccumulatorPolicy, DoubleDouble, as_policy, dd_add
 
@@ -120,6 +121,11 @@ def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = Fal
         if kind == KIND_REAL:
             vals = _real_batch([ms[i] for i in idx], policy, device, exact, stats)
             for i, v in zip(idx, vals):
+                out[i] = v
+        elif kind == KIND_INT:
+            from .integer import int_batch_totals
+            ds = [sparse_to_dense(ms[i]) if isinstance(ms[i], SparsePair) else ms[i] for i in idx]
+            for i, v in zip(idx, int_batch_totals(ds, device, stats)):
                 out[i] = v
         elif kind == KIND_COMPLEX and n <= 40:
             if policy is not AccumulatorPolicy.DD:

@@ -325,6 +325,25 @@ int dispatch_c128(int n, const pk::C128Launch& a) {
   }
 }
 
+int dispatch_int_batch(int n, const pk::IntBatchLaunch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_int_batch<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40) PK_CASE(41) PK_CASE(42) PK_CASE(43) PK_CASE(44) PK_CASE(45)
+    PK_CASE(46) PK_CASE(47) PK_CASE(48) PK_CASE(49) PK_CASE(50) PK_CASE(51) PK_CASE(52)
+    PK_CASE(53) PK_CASE(54) PK_CASE(55) PK_CASE(56) PK_CASE(57) PK_CASE(58) PK_CASE(59)
+    PK_CASE(60) PK_CASE(61) PK_CASE(62) PK_CASE(63)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
 int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
   switch (n) {
 #define PK_CASE(N) \
@@ -1403,6 +1422,84 @@ int pk_dd_accumulate(const double* vals, int64_t count, double out[2]) {
     for (int64_t k = 0; k < count; ++k) acc = h_dd_add(acc, dd_t{vals[k], 0.0});
     out[0] = acc.hi;
     out[1] = acc.lo;
+  });
+}
+
+int pk_int_batch(const int64_t* a, int n, int batch, int device, uint64_t* out_z,
+                 pk_int_info* info, pk_run_stats* stats) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    check_n(n);
+    if (batch < 0) fail(PK_ERR_ARG, "negative batch");
+    if (batch == 0) return;
+    if (!a || !out_z) fail(PK_ERR_ARG, "null pointer argument");
+    const size_t nn = (size_t)n * n, nc = (size_t)(n > 1 ? n - 1 : 0) * n;
+    std::vector<int> hcols(nc * batch), hz0((size_t)n * batch);
+    int zb = 5;
+    for (int b = 0; b < batch; ++b) {
+      IntPrep ip = prep_int(a + nn * b, n);
+      if (!ip.exact_terms)
+        fail(PK_ERR_OVERFLOW, "batched integer walk: a term may reach 2^127 (matrix " +
+                                  std::to_string(b) + ")");
+      if (nc) std::memcpy(hcols.data() + nc * b, ip.zcols.data(), nc * sizeof(int));
+      std::memcpy(hz0.data() + (size_t)n * b, ip.z0.data(), (size_t)n * sizeof(int));
+      if (ip.zb > zb) zb = ip.zb;
+      if (info) fill_info(ip, info + b);
+    }
+    DevCtx& c = dev_ctx(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const size_t ints = ((nc + n) * batch + 3) & ~size_t(3);
+    ensure(c.scratch, c.scratch_cap, ints * 4 + 64);
+    int* d_cols = (int*)c.scratch;
+    int* d_z0 = d_cols + nc * batch;
+    if (nc) ck(cudaMemcpyAsync(d_cols, hcols.data(), nc * batch * 4, cudaMemcpyHostToDevice, c.stream), "H2D cols");
+    ck(cudaMemcpyAsync(d_z0, hz0.data(), (size_t)n * batch * 4, cudaMemcpyHostToDevice, c.stream), "H2D z0");
+    // i192 outputs in the dd workspaces (24 B <= 32 B per dd pair)
+    ensure(c.chunks, c.chunks_cap, (size_t)batch);
+    ck(cudaEventRecord(c.e0, c.stream), "event record");
+    int k = 0;
+    if (n >= pk::kIntNMin) {
+      k = pk::batch_log2_chunk(n, pk::int_logu(n));
+      const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
+      ensure(c.groups, c.groups_cap, groups * batch);
+      pk::IntBatchLaunch l{};
+      l.d_cols = d_cols;
+      l.d_z0 = d_z0;
+      l.zb = zb;
+      l.batch = batch;
+      l.k = k;
+      l.group_part = c.groups;
+      l.out = c.chunks;
+      l.stream = c.stream;
+      l.sms = c.sms;
+      ck((cudaError_t)dispatch_int_batch(n, l), "int batch launch");
+    } else {
+      const unsigned grid = (unsigned)((batch + 127) / 128);
+      pk::walk_int_multi<<<grid, 128, 0, c.stream>>>(d_cols, d_z0, n, batch, (pk::i192*)c.chunks);
+      ck(cudaGetLastError(), "walk_int_multi launch");
+    }
+    ck(cudaEventRecord(c.e1, c.stream), "event record");
+    ck(cudaStreamSynchronize(c.stream), "kernel execution");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c.e0, c.e1), "event time");
+    std::vector<pk::i192> hv((size_t)batch);
+    ck(cudaMemcpy(hv.data(), c.chunks, (size_t)batch * sizeof(pk::i192), cudaMemcpyDeviceToHost), "D2H");
+    for (int b = 0; b < batch; ++b) {
+      out_z[3 * b] = hv[b].w0;
+      out_z[3 * b + 1] = hv[b].w1;
+      out_z[3 * b + 2] = hv[b].w2;
+    }
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->kernel_ms = ms;
+      stats->iterates = total_iterates(n) * (uint64_t)batch;
+      stats->log2_chunk = k;
+      stats->devices = 1;
+      stats->launches = 1;
+      stats->wall_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
   });
 }
 

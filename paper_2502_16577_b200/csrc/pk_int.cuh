@@ -184,16 +184,16 @@ struct IntSteps<N, C, U, U> {
 };
 
 template <int N, class C>
-__device__ __forceinline__ i192 int_walk_chunk(const IntParams<N>& p, const int* scols, uint64_t c) {
+__device__ __forceinline__ i192 int_walk_chunk(const int* z0, int k, uint64_t g_end,
+                                               const int* scols, uint64_t c) {
   constexpr int LOGU = C::LOGU;
   constexpr int U = 1 << LOGU;
   constexpr int NP = int_stride<N>();
   IntWalk<N, C> w;
   w.scols = scols;
-  const int k = p.k;
   const uint64_t base = c << k;
 #pragma unroll
-  for (int i = 0; i < N; ++i) w.z[i] = p.z0[i];
+  for (int i = 0; i < N; ++i) w.z[i] = z0[i];
   const uint64_t code = base ^ (base >> 1);
   for (int j = 0; j < N - 1; ++j)
     if ((code >> j) & 1ull) w.template update_static<1>(scols + j * NP);
@@ -204,7 +204,7 @@ __device__ __forceinline__ i192 int_walk_chunk(const IntParams<N>& p, const int*
     const int jz = (int)(m >> 62);
     IntSteps<N, C, 1, U>::run(w, s_mid, jz);
     const uint64_t g = gb + U;
-    if (m + 1 < nbody || g <= p.g_end) {
+    if (m + 1 < nbody || g <= g_end) {
       const int j = changed_col(g);
       w.update(scols + j * NP, flip_on(g, j) ? 1 : -1);
       w.fold(false);
@@ -261,12 +261,57 @@ __global__ void __launch_bounds__(kIntBlock, C::MINB) int_chunks(const __grid_co
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
     const uint64_t c = p.chunk_lo + grp * 32 + lane;
-    i192 part = int_walk_chunk<N, C>(p, scols, c);
+    i192 part = int_walk_chunk<N, C>(p.z0, p.k, p.g_end, scols, c);
     if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
     part = warp_sum_i192(part);
     if (lane == 0) p.group_part[grp] = part;
   }
   grid_tail_sum_i192<kIntBlock>(p.group_part, p.num_groups, p.out, p.counter);
+}
+
+// batched whole walks of `batch` integer matrices of order N (decomposition
+// leaves): one block per matrix at a time, 2^(N-1-k) aligned chunks per
+// matrix; the matrix total is an exact sum, so any order gives its value
+template <int N>
+struct IntBatchParams {
+  const int* cols;  // [batch][(N-1)*N] z-space column steps
+  const int* z0;    // [batch][N]
+  i192* group_part; // [batch][groups] scratch
+  i192* out;        // [batch] z-space partial over [1, 2^(N-1)-1]
+  int batch;
+  int k;
+};
+
+template <int N, class C>
+__global__ void __launch_bounds__(kIntBlock, C::MINB) int_batch(const __grid_constant__ IntBatchParams<N> p) {
+  constexpr int NP = int_stride<N>();
+  __shared__ __align__(16) int scols[(N - 1) * NP];
+  __shared__ int sz0[N];
+  const uint64_t total = (1ull << (N - 1)) - 1;
+  const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    __syncthreads();
+    const int* cb = p.cols + (size_t)b * (N - 1) * N;
+    for (int t = threadIdx.x; t < (N - 1) * NP; t += blockDim.x) {
+      const int j = t / NP, i = t % NP;
+      scols[t] = (i < N) ? cb[j * N + i] : 0;
+    }
+    for (int t = threadIdx.x; t < N; t += blockDim.x) sz0[t] = p.z0[(size_t)b * N + t];
+    __syncthreads();
+    i192* gp = p.group_part + (size_t)b * groups;
+    for (int grp = wib; grp < groups; grp += wpb) {
+      i192 part = int_walk_chunk<N, C>(sz0, p.k, total, scols, (uint64_t)grp * 32 + lane);
+      part = warp_sum_i192(part);
+      if (lane == 0) gp[grp] = part;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      i192 s{0ull, 0ull, 0ull};
+      for (int g = 0; g < groups; ++g) i192_add(s, gp[g]);
+      p.out[b] = s;
+    }
+  }
 }
 
 }  // namespace pk

@@ -50,6 +50,44 @@ int launch_int(const IntLaunch& a) {
   }
 }
 
+template <int N, class C>
+static int launch_int_batch_cfg(const IntBatchLaunch& a) {
+  auto kern = int_batch<N, C>;
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kIntBlock, 0);
+    if (e != cudaSuccess) return (int)e;
+    occ = o > 0 ? o : 1;
+  }
+  IntBatchParams<N> p;
+  p.cols = a.d_cols;
+  p.z0 = a.d_z0;
+  p.group_part = (i192*)a.group_part;
+  p.out = (i192*)a.out;
+  p.batch = a.batch;
+  p.k = a.k;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if ((uint64_t)a.batch < grid) grid = a.batch;
+  kern<<<(unsigned)grid, kIntBlock, 0, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_int_batch(const IntBatchLaunch& a) {
+  constexpr int L = int_logu(N);
+  constexpr int MB = int_minb(N);
+  switch (a.zb) {
+    case 5: return launch_int_batch_cfg<N, IntCfg<5, L, MB>>(a);
+    case 7: return launch_int_batch_cfg<N, IntCfg<7, L, MB>>(a);
+    case 15: return launch_int_batch_cfg<N, IntCfg<15, L, MB>>(a);
+    case 31: return launch_int_batch_cfg<N, IntCfg<31, L, MB>>(a);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace pk
 
-#define PK_INSTANTIATE_INT(N) template int pk::launch_int<N>(const pk::IntLaunch&);
+#define PK_INSTANTIATE_INT(N)                                \
+  template int pk::launch_int<N>(const pk::IntLaunch&); \
+  template int pk::launch_int_batch<N>(const pk::IntBatchLaunch&);

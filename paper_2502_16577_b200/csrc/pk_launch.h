@@ -130,4 +130,20 @@ struct IntLaunch {
 template <int N>
 int launch_int(const IntLaunch& a);
 
+// batched whole integer walks of `batch` matrices of order N (device inputs)
+struct IntBatchLaunch {
+  const int* d_cols;   // [batch][(N-1)*N]
+  const int* d_z0;     // [batch][N]
+  int zb;              // max over the batch
+  int batch;
+  int k;
+  void* group_part;    // i192 [batch][2^(N-1-k)/32]
+  void* out;           // i192 [batch]
+  cudaStream_t stream;
+  int sms;
+};
+
+template <int N>
+int launch_int_batch(const IntBatchLaunch& a);
+
 }  // namespace pk

@@ -195,6 +195,30 @@ __global__ void __launch_bounds__(kWalkBlock)
 // range walker: run-time n, exact product by repeated 128-bit wrapping
 // multiply (exact under the same host bound), one thread per range
 
+// whole exact walks of `batch` small integer matrices, one thread each
+// (batched API for n < 11): out[r] = z-space partial over [1, 2^(n-1)-1]
+__global__ void __launch_bounds__(128)
+    walk_int_multi(const int* __restrict__ cols, const int* __restrict__ z0, int n, int batch,
+                   i192* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= batch) return;
+  const int* cr = cols + (size_t)r * (n - 1) * n;
+  int z[64];
+  for (int i = 0; i < n; ++i) z[i] = z0[(size_t)r * n + i];
+  i192 acc{0ull, 0ull, 0ull};
+  const uint64_t end = (1ull << (n - 1)) - 1;
+  for (uint64_t g = 1; g <= end; ++g) {
+    const int j = changed_col(g);
+    const int s = flip_on(g, j) ? 1 : -1;
+    for (int i = 0; i < n; ++i) z[i] += s * cr[j * n + i];
+    unsigned __int128 p = 1;
+    for (int i = 0; i < n; ++i) p *= (unsigned __int128)(__int128)z[i];
+    const unsigned long long lo = (unsigned long long)p, hi = (unsigned long long)(p >> 64);
+    if (g & 1ull) i192_sub128(acc, lo, hi); else i192_add128(acc, lo, hi);
+  }
+  out[r] = acc;
+}
+
 __global__ void __launch_bounds__(128)
     walk_int(const int* __restrict__ cols, const int* __restrict__ z0, int n,
              const unsigned long long* __restrict__ starts,

@@ -150,6 +150,31 @@ def int_walk_total(m, devices=None, stats=None, sparse: Optional[bool] = None) -
     return finalize_int(total_z << info.even_rows, n)
 
 
+def int_batch_totals(ms, device: int = 0, stats=None) -> List[int]:
+    """Exact permanents of many integer matrices of one order in one launch
+    (pk_int_batch); matrices whose terms may reach 2^127 are walked one by
+    one (int_walk_total's modular route)."""
+    if not ms:
+        return []
+    probs = [IntProblem(m) for m in ms]
+    n = probs[0].n
+    a = np.ascontiguousarray(np.concatenate([p.a for p in probs]))
+    out = np.zeros(3 * len(probs), dtype=np.uint64)
+    infos = (IntInfo * len(probs))()
+    st = stats if stats is not None else nat.RunStats()
+    lib = nat.load()
+    rc = lib.pk_int_batch(a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n, len(probs), device,
+                          nat.u64ptr(out), ctypes.cast(infos, ctypes.c_void_p), st)
+    if rc == nat.PK_ERR_OVERFLOW:
+        return [int_walk_total(m, [device], sparse=False) for m in ms]
+    nat.check(rc, "pk_int_batch")
+    res = []
+    for b, p in enumerate(probs):
+        z = _signed([int(w) for w in out[3 * b:3 * b + 3]], 192)
+        res.append(finalize_int(p.p0_y() + p.z_to_y(z, infos[b]), n))
+    return res
+
+
 EXACT_WALKER_LIMIT = 1 << 20
 
 

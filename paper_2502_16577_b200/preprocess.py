@@ -488,6 +488,7 @@ class _LeafQueue:
     """Kernel leaves waiting for a batched device evaluation."""
 
     def __init__(self, kind: str, policy: AccumulatorPolicy, device: int, stats: DecompStats):
+        # kind/policy/device of the whole tree; leaves of every order queue here
         self.kind, self.policy, self.device, self.stats = kind, policy, device, stats
         self.items: List[Tuple[int, Scalar, SparsePair]] = []
 
@@ -504,11 +505,16 @@ class _LeafQueue:
         from .matrix import sparse_to_dense
         items, self.items = self.items, []
         if self.kind == KIND_INT:
-            for (tid, mult, m) in items:
-                # dense exact kernel: no per-leaf code generation
-                out.append((tid, mult * int_walk_total(sparse_to_dense(m), [self.device],
-                                                       sparse=False)))
+            from .integer import int_batch_totals
+            by_n: Dict[int, List[int]] = defaultdict(list)
+            for k, (_, _, m) in enumerate(items):
+                by_n[m.n].append(k)
+            for n, idx in by_n.items():
+                vals = int_batch_totals([sparse_to_dense(items[k][2]) for k in idx], self.device)
                 self.stats.leaf_launches += 1
+                for k, v in zip(idx, vals):
+                    tid, mult, _ = items[k]
+                    out.append((tid, mult * v))
             return
         groups: Dict[int, List[int]] = defaultdict(list)
         for k, (_, _, m) in enumerate(items):
@@ -689,11 +695,13 @@ def _evaluate_native_leaves(leaves, kind, policy, device, stats, contribs) -> No
     from .matrix import DenseMatrix
     for m, (ids, mults, mats) in sorted(leaves.items()):
         if kind == KIND_INT:
-            for tid, mult, rows in zip(ids, mults, mats):
-                v = int_walk_total(DenseMatrix.from_rows(rows, kind=KIND_INT), [device],
-                                   sparse=False)
-                contribs.append((tid, mult * v))
+            from .integer import int_batch_totals
+            for lo in range(0, len(ids), LEAF_BATCH):
+                vals = int_batch_totals([DenseMatrix.from_rows(r, kind=KIND_INT)
+                                         for r in mats[lo:lo + LEAF_BATCH]], device)
                 stats.leaf_launches += 1
+                for tid, mult, v in zip(ids[lo:lo + LEAF_BATCH], mults[lo:lo + LEAF_BATCH], vals):
+                    contribs.append((tid, mult * v))
             continue
         for lo in range(0, len(ids), LEAF_BATCH):
             chunk = mats[lo:lo + LEAF_BATCH]

@@ -96,3 +96,20 @@ def test_complex_batch_small_orders_and_tolerance(golden):
     for g, m in zip(pk.permanent_batch(ms), ms):
         ref = pk.perm_nw(m)
         assert abs(g - ref) <= 1e-10 * abs(ref)
+
+
+@pytest.mark.parametrize("n", [6, 11, 18, 24])
+def test_integer_batch_is_exact_and_one_launch(n):
+    # one pk_int_batch launch for many integer matrices: every permanent
+    # equals the single-matrix exact walk (and the reference's integer rule)
+    from paper_2502_16577_b200.integer import int_batch_totals, int_walk_total
+    rng = np.random.default_rng(n)
+    ms = [pk.DenseMatrix.from_rows(rng.integers(-3, 4, size=(n, n)).tolist(), kind="integer")
+          for _ in range(6)]
+    ms.append(pk.random_binary(n, 5, 0.4))
+    st = _native.RunStats()
+    got = int_batch_totals(ms, 0, st)
+    for m, g in zip(ms, got):
+        assert g == int_walk_total(m, [0], sparse=False)
+    assert st.launches == 1
+    assert pk.permanent_batch(ms) == got

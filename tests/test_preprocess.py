@@ -183,8 +183,8 @@ def test_decomp_run_matches_reference_value(name):
         assert abs(got - want) <= 1e-10 * abs(want) + 1e-300, (got, want)
     assert st.kernel_leaves == gold["stats"]["kernel_leaves"]
     if st.kernel_leaves:
-        assert st.leaf_launches <= max(1, st.kernel_leaves if kind == "integer"
-                                       else len(set(st.leaf_sizes)))
+        # one batched launch per leaf order (every kind)
+        assert st.leaf_launches <= len(set(st.leaf_sizes))
 
 
 @pytest.mark.gpu
