@@ -392,7 +392,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     for (int j = 0; j < n - 1; ++j)
       for (size_t t = 0; t < sp->rows[j].size(); ++t)
         kd.input[voff + off[j] + t] = cols[(size_t)j * n + sp->rows[j][t]];
-    kd.logu = pk::spa_f64_logu(n);
+    kd.logu = pk::spa_f64_logu(n);  // planning as K1 (the kernel needs k > its own body length)
     kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                   uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
       pk::SpaF64Launch a{};

@@ -77,13 +77,20 @@ __device__ __forceinline__ double row_product(const double (&x)[N]) {
 //        register count is not a divisor-friendly number)
 //   FA   fused accumulate (with BA): the last product multiply and the body
 //        sum become one DFMA, bsum = fma(+-p', x[n-1], bsum)
+//   QF   fast QQ (POL_QQ, not bit-identical): the double-double product
+//        keeps (hi, lo) unnormalised -- hi' = hi*x, lo' = fma(lo, x,
+//        fma(hi, x, -hi')) -- 3 FP64 ops per row instead of qq_mul_step's 7;
+//        the body's terms are summed with a two_sum on the hi parts plus a
+//        plain sum of the lo parts and folded once per body into the
+//        double-double partial
 template <int POL_, int PS_, int LOGU_, bool BA_, int MINB_ = 1, int BLOCK_ = 128,
-          bool FA_ = false>
+          bool FA_ = false, bool QF_ = false>
 struct DenseCfg {
   static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, MINB = MINB_;
   static constexpr int BLOCK = BLOCK_;
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
   static constexpr bool FA = FA_ && BA;
+  static constexpr bool QF = QF_ && POL_ == POL_QQ;
 };
 
 template <int N>
@@ -95,6 +102,7 @@ struct DenseWalk {
   double x[N];
   Acc<C::POL> acc;
   double bsum;
+  double qs, qc, ql;  // fast-QQ body sums: hi parts (two_sum s + c), lo parts
 
   __device__ __forceinline__ explicit DenseWalk(const double* s_) : scols(s_) {}
 
@@ -151,7 +159,30 @@ struct DenseWalk {
 
   // fold the current state's signed product (term sign = iterate parity)
   __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
-    if constexpr (C::POL == POL_QQ) {
+    if constexpr (C::QF) {
+      double hi = __dmul_rn(x[0], x[1]);
+      double lo = __fma_rn(x[0], x[1], -hi);
+#pragma unroll
+      for (int i = 2; i < N; ++i) {
+        const double h2 = __dmul_rn(hi, x[i]);
+        lo = __fma_rn(lo, x[i], __fma_rn(hi, x[i], -h2));
+        hi = h2;
+      }
+      if (odd) {
+        hi = -hi;
+        lo = -lo;
+      }
+      if (first_in_body) {
+        qs = hi;
+        qc = 0.0;
+        ql = lo;
+      } else {
+        double e;
+        two_sum(qs, hi, qs, e);
+        qc = __dadd_rn(qc, e);
+        ql = __dadd_rn(ql, lo);
+      }
+    } else if constexpr (C::POL == POL_QQ) {
       double ph = 1.0, pl = 0.0;
 #pragma unroll
       for (int i = 0; i < N; ++i) qq_mul_step(ph, pl, x[i]);
@@ -177,6 +208,7 @@ struct DenseWalk {
 
   __device__ __forceinline__ void end_body() {
     if constexpr (C::BA) acc.add(bsum);
+    if constexpr (C::QF) acc.add2(qs, __dadd_rn(qc, ql));
   }
 };
 

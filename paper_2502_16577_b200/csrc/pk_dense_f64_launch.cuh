@@ -60,7 +60,8 @@ int launch_dense_f64(const DenseLaunch& a) {
       return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, MB, 128, true>>(a, p);
     case POL_QQ:
-      return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p);
+      return a.exact ? launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p)
+                     : launch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true>>(a, p);
     default:
       return (int)cudaErrorInvalidValue;
   }
@@ -105,7 +106,8 @@ int launch_dense_f64_batch(const DenseBatchLaunch& a) {
       return a.exact ? launch_batch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a)
                      : launch_batch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, MB, 128, true>>(a);
     case POL_QQ:
-      return launch_batch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a);
+      return a.exact ? launch_batch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a)
+                     : launch_batch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true>>(a);
     default:
       return (int)cudaErrorInvalidValue;
   }

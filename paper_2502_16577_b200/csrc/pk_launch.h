@@ -17,6 +17,9 @@ constexpr int kDenseNMax = 63;
 // resident 128-thread blocks per SM up to N = 36, two above.
 constexpr int dense_logu(int N) { return N <= 50 ? 4 : 3; }
 constexpr int dense_minb(int N) { return N <= 36 ? 3 : 2; }
+// fast QQ (DenseCfg::QF) carries two registers per product chain: shorter
+// bodies (profiles/r01_qf_sweep.txt)
+constexpr int qf_logu(int N) { return N <= 36 ? 2 : 3; }
 
 struct DenseLaunch {
   const double* cols;   // host, (n-1)*n

@@ -69,8 +69,11 @@ struct SpaF64Launch {
 
 int spa_f64_launch(const SpaF64Spec& sp, const SpaF64Launch& a, std::string& err);
 std::string spa_f64_source(const SpaF64Spec& sp);
-// body length (log2) of the generated sparse real kernel for order n
-constexpr int spa_f64_logu(int n) { return n <= 50 ? 4 : 3; }
+// body length (log2) of the generated sparse real kernel for order n: K1's
+// (dense_logu), or qf_logu for fast QQ, so the two stay bit-identical
+constexpr int spa_f64_logu(int n, bool fast_qq = false) {
+  return fast_qq ? (n <= 36 ? 2 : 3) : (n <= 50 ? 4 : 3);
+}
 
 // ---------------------------------------------------------- sparse complex
 // Per-pattern generated kernel for the sparse complex walk (chunk_sparse_c128,

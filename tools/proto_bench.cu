@@ -130,14 +130,19 @@ int main(int argc, char** argv) {
   V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, BL, FA>>(NM, h##NN, KK, GL, R); }}
 #define SVAR(NM, NN, UX, MB, KK, GL, R) \
   V{NM, [] { run_variant<NN, DenseCfg<POL_KAHAN, 1, UX, true, MB, 128, true>, true>(NM, h##NN, KK, GL, R); }}
+#define QVAR(NM, NN, UX, MB, KK, GL, R) \
+  V{NM, [] { run_variant<NN, DenseCfg<POL_QQ, 1, UX, false, MB, 128, false, true>>(NM, h##NN, KK, GL, R); }}
   std::vector<V> vs = {
-    VAR("40_k15", 40, 4, 2, 128, true, 15, 0, 2),
-    VAR("40_k17", 40, 4, 2, 128, true, 17, 0, 2),
-    VAR("40_k19", 40, 4, 2, 128, true, 19, 0, 2),
-    VAR("40_k21", 40, 4, 2, 128, true, 21, 0, 2),
-    VAR("36_k13", 36, 4, 3, 128, true, 13, 0, 3),
-    VAR("36_k15", 36, 4, 3, 128, true, 15, 0, 3),
-    VAR("36_k17", 36, 4, 3, 128, true, 17, 0, 3),
+    VAR("36_kahan_fa", 36, 4, 3, 128, true, 14, 0, 2),
+    QVAR("36_qf_u4_mb3", 36, 4, 3, 14, 0, 2),
+    QVAR("36_qf_u4_mb2", 36, 4, 2, 14, 0, 2),
+    QVAR("36_qf_u3_mb3", 36, 3, 3, 14, 0, 2),
+    QVAR("36_qf_u3_mb2", 36, 3, 2, 14, 0, 2),
+    QVAR("36_qf_u2_mb3", 36, 2, 3, 14, 0, 2),
+    QVAR("40_qf_u4_mb2", 40, 4, 2, 17, 0, 1),
+    QVAR("40_qf_u3_mb2", 40, 3, 2, 17, 0, 1),
+    QVAR("48_qf_u3_mb2", 48, 3, 2, 20, 4736, 1),
+    QVAR("48_qf_u4_mb2", 48, 4, 2, 20, 4736, 1),
   };
   for (auto& v : vs) {
     bool sel = argc < 2;
