@@ -69,11 +69,21 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        # PK_BENCH_SHARE_GPU=1: validation mode for boxes with fewer GPUs than
+        # ranks -- ranks share devices round robin and gather over gloo (the
+        # numbers are then not a scaling measurement)
+        self.shared = os.environ.get("PK_BENCH_SHARE_GPU") == "1"
+        self.device = self.local
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.shared:
+                self.device = self.local % max(1, torch.cuda.device_count())
+                torch.cuda.set_device(self.device)
+                dist.init_process_group("gloo")
+            else:
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
 
     def barrier(self):
@@ -85,7 +95,8 @@ class Dist:
         if not self.pg:
             return [list(vals)]
         import torch
-        t = torch.tensor(list(vals), dtype=torch.float64, device=f"cuda:{self.local}")
+        dev = "cpu" if self.shared else f"cuda:{self.local}"
+        t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.pg.all_gather(out, t)
         return [o.cpu().tolist() for o in out]
@@ -435,8 +446,8 @@ def run_b200(args, dist: Dist):
     else:
         from paper_2502_16577_b200.distributed import rank_span
         lo, hi = rank_span(n, rank, N)
-    dev = [dist.local]
-    flusher = L2Flusher(dist.local)
+    dev = [dist.device]
+    flusher = L2Flusher(dist.device)
 
     def step_e2e():
         t0 = time.perf_counter()
@@ -451,8 +462,8 @@ def run_b200(args, dist: Dist):
         step_e2e()
     sync_device()
 
-    peak_tf = _native.fp64_peak_tflops(dist.local)
-    clocks = ClockSampler(dist.local)
+    peak_tf = _native.fp64_peak_tflops(dist.device)
+    clocks = ClockSampler(dist.device)
     clocks.start()
     kernel_ms, wall_ms, launches = [], [], 0
     for _ in range(args.steps):
@@ -519,7 +530,7 @@ def run_b200(args, dist: Dist):
         inst = ncu_metric(wl.kind, "smsp__inst_executed.sum")
         upl = ncu_metric(wl.kind, "updates_per_launch")
         sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
-        peak_gi = 4 * _native_sms(dist.local) * sm_mhz * 1e-3
+        peak_gi = 4 * _native_sms(dist.device) * sm_mhz * 1e-3
         ipu = inst / upl * 32 if inst and upl else None  # thread-level instr / update
         ach = ups / N * ipu / 32 * 1e-9 if ipu else None
         roofline = {"bound": "issue", "achieved": ach, "peak": peak_gi, "unit": "Gwarp-inst/s",
@@ -543,6 +554,7 @@ def run_b200(args, dist: Dist):
         "wall_ms_per_step": statistics.mean(step_w),
         "higher_is_better": True,
         "scaling": "strong",
+        **({"validation_only": "PK_BENCH_SHARE_GPU=1: ranks shared GPUs"} if dist.shared else {}),
         "vs_baseline": ups / PAPER_N40_UPS if (n == 40 and wl.kind == "dense") else None,
         "vs_baseline_ref": "SUperman best kernel on a Quadro GV100, n=40 in 14.17 s "
                            "(PAPER.md:785) = 3.88e10 updates/s",

@@ -7,6 +7,7 @@
 // (one tree-reduced double-double per device), the unaligned head and tail
 // to the range walkers; the host combines the pieces in a fixed order.
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -360,6 +361,16 @@ int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
   }
 }
 
+// state rebuild period of the fast real walks (pk_launch.h); the
+// PK_REBUILD_LOG2 environment variable overrides it (0 = off) for A/B runs
+int rebuild_log2() {
+  static const int v = [] {
+    const char* e = getenv("PK_REBUILD_LOG2");
+    return e ? atoi(e) : pk::kDenseRebuildLog2;
+  }();
+  return v;
+}
+
 size_t ncols_of(int n) { return (size_t)(n > 1 ? n - 1 : 1) * n; }
 
 Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact,
@@ -396,6 +407,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                   uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
       pk::SpaF64Launch a{};
+      a.rb = rebuild_log2();
       a.d_cols = d_in;
       a.d_x0 = d_in + nc;
       a.d_vals = d_in + voff;
@@ -423,6 +435,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     a.policy = policy;
     a.exact = exact;
     a.k = k;
+    a.rb = rebuild_log2();
     a.chunk_lo = chunk_lo;
     a.num_groups = groups;
     a.g_end = g_end;
@@ -1206,6 +1219,7 @@ int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, i
       a.exact = (flags & PK_FLAG_EXACT) != 0;
       a.batch = batch;
       a.k = k;
+      a.rb = rebuild_log2();
       a.group_part = c.groups;
       a.out = c.chunks;
       a.stream = c.stream;

@@ -38,6 +38,7 @@ struct DenseF64Params {
   unsigned long long num_groups;  // groups of 32 consecutive chunks
   unsigned long long g_end;       // inclusive last iterate of the walk
   int k;                          // log2 chunk size, k > LOGU
+  int rb;                         // state rebuild period (log2 steps), 0 = none
 };
 
 template <int N, int PS>
@@ -157,6 +158,50 @@ struct DenseWalk {
     }
   }
 
+  // Periodic state rebuild (fast modes): every 2^rb
+  // steps x is recomputed from scratch instead of carrying the rounding of
+  // all earlier incremental updates. The chunk-constant part -- x0 plus the
+  // columns of gray(base) at bits >= k -- is stashed once per chunk in shared
+  // memory (one slot per thread, stride BLOCK); a rebuild adds the columns of
+  // the iterate's Gray bits below k to it.
+  __device__ __forceinline__ void stash_high(const double* x0, uint64_t base, int k,
+                                             double* sxs) {
+    constexpr int NP = smem_stride<N>();
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x0[i];
+    // set Gray bits >= k, ascending (ffs walk: one iteration per column)
+    for (uint64_t code = ((base ^ (base >> 1)) >> k) << k; code; code &= code - 1) {
+      const int j = __ffsll((long long)code) - 1;
+      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const double2 v = c2[i / 2];
+        x[i] = __dadd_rn(x[i], v.x);
+        if (i + 1 < N) x[i + 1] = __dadd_rn(x[i + 1], v.y);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) sxs[i * C::BLOCK] = x[i];
+  }
+
+  __device__ __forceinline__ void rebuild(uint64_t g, int k, const double* sxs) {
+    constexpr int NP = smem_stride<N>();
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = sxs[i * C::BLOCK];
+    // set Gray bits < k, ascending (warp-uniform: g is the same for all lanes
+    // up to the chunk base, whose bits < k are zero)
+    for (uint64_t code = (g ^ (g >> 1)) & ((1ull << k) - 1); code; code &= code - 1) {
+      const int j = __ffsll((long long)code) - 1;
+      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const double2 v = c2[i / 2];
+        x[i] = __dadd_rn(x[i], v.x);
+        if (i + 1 < N) x[i + 1] = __dadd_rn(x[i + 1], v.y);
+      }
+    }
+  }
+
   // fold the current state's signed product (term sign = iterate parity)
   __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
     if constexpr (C::QF) {
@@ -241,17 +286,23 @@ struct StaticSteps<N, C, U, U> {
 
 // Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
 // g_end); returns its normalised partial (parallel.py:282-289).
+// rb > 0 (fast modes): the state is rebuilt from the stash sxs every 2^rb
+// steps (rb >= LOGU); rb = 0 walks the chunk incrementally like the reference.
 template <int N, class C>
 __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0, int k,
-                                           uint64_t g_end, uint64_t c) {
+                                           uint64_t g_end, uint64_t c, int rb = 0,
+                                           double* sxs = nullptr) {
   constexpr int LOGU = C::LOGU;
   constexpr int U = 1 << LOGU;
   DenseWalk<N, C> w(scols);
   const uint64_t base = c << k;
-  w.jump_in(x0, base);
+  const uint64_t rb_mask = rb > 0 ? (1ull << (rb - LOGU)) - 1 : ~0ull;
+  if (rb > 0) w.stash_high(x0, base, k, sxs);
+  else w.jump_in(x0, base);
   const uint64_t nbody = 1ull << (k - LOGU);
   for (uint64_t m = 0; m < nbody; ++m) {
     const uint64_t gb = base + (m << LOGU);
+    if (rb > 0 && (m & rb_mask) == 0) w.rebuild(gb, k, sxs);
     const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
     const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
     StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
@@ -278,10 +329,16 @@ __device__ __forceinline__ void stage_columns(double* scols, const double* cols)
   }
 }
 
+template <int N>
+__host__ __device__ constexpr size_t dense_cols_doubles() {
+  return (size_t)(N - 1) * smem_stride<N>();
+}
+
 template <int N, class C>
 __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_f64_chunks(const __grid_constant__ DenseF64Params<N> p) {
   extern __shared__ __align__(16) double scols[];
+  double* sxs = scols + dense_cols_doubles<N>() + threadIdx.x;  // rebuild stash
   stage_columns<N>(scols, p.cols);
   __syncthreads();
   const unsigned int lane = threadIdx.x & 31u;
@@ -289,7 +346,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
     const uint64_t c = p.chunk_lo + grp * 32 + lane;
-    dd_t part = walk_chunk<N, C>(scols, p.x0, p.k, p.g_end, c);
+    dd_t part = walk_chunk<N, C>(scols, p.x0, p.k, p.g_end, c, p.rb, sxs);
     if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
     part = warp_tree_dd(part);
     if (lane == 0) p.group_part[grp] = part;
@@ -316,6 +373,7 @@ struct DenseBatchParams {
   dd_t* out;            // [batch] partial over [1, 2^(N-1)-1]
   int batch;
   int k;
+  int rb;               // state rebuild period (log2 steps), 0 = none
 };
 
 template <int N, class C>
@@ -324,6 +382,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
   extern __shared__ __align__(16) double smem[];
   double* scols = smem;
   double* sx0 = smem + (N - 1) * smem_stride<N>();
+  double* sxs = sx0 + N + threadIdx.x;  // rebuild stash (stride BLOCK)
   const uint64_t total = (1ull << (N - 1)) - 1;
   const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -334,7 +393,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     __syncthreads();
     dd_t* gp = p.group_part + (size_t)b * groups;
     for (int grp = wib; grp < groups; grp += wpb) {
-      dd_t part = walk_chunk<N, C>(scols, sx0, p.k, total, (uint64_t)grp * 32 + lane);
+      dd_t part = walk_chunk<N, C>(scols, sx0, p.k, total, (uint64_t)grp * 32 + lane, p.rb, sxs);
       part = warp_tree_dd(part);
       if (lane == 0) gp[grp] = part;
     }

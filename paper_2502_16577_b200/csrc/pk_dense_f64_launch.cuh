@@ -11,7 +11,8 @@ namespace pk {
 template <int N, class C>
 static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
   auto kern = dense_f64_chunks<N, C>;
-  constexpr size_t smem = dense_smem_bytes<N>();
+  // columns + the per-thread rebuild stash (fast modes)
+  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * C::BLOCK;
   static int occ = -1;  // per instantiation; every B200 gives the same answer
   if (occ < 0) {
     if (smem > 48 * 1024) {
@@ -49,6 +50,7 @@ int launch_dense_f64(const DenseLaunch& a) {
   p.num_groups = a.num_groups;
   p.g_end = a.g_end;
   p.k = a.k;
+  p.rb = a.exact ? 0 : a.rb;
   switch (a.policy) {
     case POL_DD:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
@@ -70,9 +72,14 @@ int launch_dense_f64(const DenseLaunch& a) {
 template <int N, class C>
 static int launch_batch_cfg(const DenseBatchLaunch& a) {
   auto kern = dense_f64_batch<N, C>;
-  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N;
+  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * (1 + C::BLOCK);
   static int occ = -1;
   if (occ < 0) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
     int o = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
     if (e != cudaSuccess) return (int)e;
@@ -85,6 +92,7 @@ static int launch_batch_cfg(const DenseBatchLaunch& a) {
   p.out = a.out;
   p.batch = a.batch;
   p.k = a.k;
+  p.rb = a.exact ? 0 : a.rb;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if ((uint64_t)a.batch < grid) grid = a.batch;
   kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);

@@ -21,12 +21,18 @@ constexpr int dense_minb(int N) { return N <= 36 ? 3 : 2; }
 // bodies (profiles/r01_qf_sweep.txt)
 constexpr int qf_logu(int N) { return N <= 36 ? 2 : 3; }
 
+// state rebuild period of the fast modes (log2 steps): x is recomputed from
+// scratch every 2^dense_rebuild_log2 steps instead of drifting over a whole
+// chunk (profiles/r01_accuracy_probe.txt)
+constexpr int kDenseRebuildLog2 = 8;
+
 struct DenseLaunch {
   const double* cols;   // host, (n-1)*n
   const double* x0;     // host, n
   int policy;
   bool exact;
   int k;                // log2 chunk size, k > dense_logu(n)
+  int rb;               // rebuild period (log2 steps) in fast mode, 0 = none
   uint64_t chunk_lo;
   uint64_t num_groups;  // groups of 32 chunks
   uint64_t g_end;
@@ -50,6 +56,7 @@ struct DenseBatchLaunch {
   bool exact;
   int batch;
   int k;
+  int rb;                // rebuild period (log2 steps) in fast mode, 0 = none
   dd_t* group_part;      // [batch][2^(N-1-k)/32]
   dd_t* out;             // [batch]
   cudaStream_t stream;

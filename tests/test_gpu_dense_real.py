@@ -19,7 +19,7 @@ import golden_io as gio
 import oracle
 import paper_2502_16577_b200 as pk
 from paper_2502_16577_b200 import kernels as K
-from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_pairwise
+from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_add, dd_pairwise
 
 pytestmark = pytest.mark.gpu
 
@@ -175,3 +175,22 @@ def test_errors_are_the_reference_classes():
     prob = K.DenseF64Problem(m)
     with pytest.raises(ValueError):
         prob.chunks(3, 0, 32, AccumulatorPolicy.DD)  # k below the body length
+
+
+def test_state_rebuild_removes_chunk_length_drift():
+    # fast mode rebuilds x every 2^8 steps: the result
+    # no longer depends on the chunk length at the 1e-10 level, where the
+    # incremental walk of 2^k-step chunks drifted by ~1e-9 (n = 36, k = 16;
+    # profiles/r01_accuracy_probe.txt)
+    n = 34
+    g = np.random.default_rng(20261017).uniform(0.0, 1.0, size=(n, n))
+    m = pk.DenseMatrix.from_array(g)
+    prob = K.DenseF64Problem(m)
+    p0 = K.policy_product(prob.x0, AccumulatorPolicy.KAHAN)
+    T = K.total_iterates(n)
+    vals = []
+    for k in (8, 12, 16, 20):
+        part = prob.walk(1, T, AccumulatorPolicy.KAHAN, log2_chunk=k)
+        vals.append(dd_add(DoubleDouble(p0, 0.0), part).hi)
+    for v in vals[1:]:
+        assert abs(v - vals[0]) <= 1e-10 * abs(vals[0]), vals
