@@ -321,27 +321,41 @@ class Workload:
             self.desc = (f"n={n} complex fp64 top-left block of a Haar U({n * n}) seed {SEED}, "
                          f"whole walk per step")
 
+    def whole_walk_log2_chunk(self):
+        """The chunk exponent the library picks for the whole walk (2^22
+        chunks for real / integer walks, 2^19 for complex; pk_abi.cu
+        plan_dense). Every rank uses it, so an N-rank split walks exactly the
+        single-GPU chunks and reproduces its bits (power-of-two N)."""
+        from paper_2502_16577_b200.csrc_params import c128_logu, dense_logu
+        n = self.n
+        if self.kind == "haar":
+            return max(c128_logu(n) + 1, (n - 1) - 19)
+        logu = 2 if self.kind == "binary" else dense_logu(n)
+        return max(logu + 1, (n - 1) - 22)
+
     def walk(self, lo, hi, devices):
         """(partial as a list of floats for the gather, stats)"""
         from paper_2502_16577_b200 import _native
         from paper_2502_16577_b200.precision import AccumulatorPolicy
         st = _native.RunStats()
+        k = self.whole_walk_log2_chunk()
         if self.kind == "dense":
             from paper_2502_16577_b200.kernels import DenseF64Problem
             p = DenseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
-                                            devices=devices, stats=st)
+                                            devices=devices, stats=st, log2_chunk=k)
             return [p.hi, p.lo], st
         if self.kind == "sparse":
             from paper_2502_16577_b200.kernels import SparseF64Problem
             p = SparseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
-                                             devices=devices, stats=st)
+                                             devices=devices, stats=st, log2_chunk=k)
             return [p.hi, p.lo], st
         if self.kind == "haar":
             from paper_2502_16577_b200.complex_walk import DenseC128Problem
-            r, i = DenseC128Problem(self.m).walk(lo, hi, devices=devices, stats=st)
+            r, i = DenseC128Problem(self.m).walk(lo, hi, devices=devices, stats=st,
+                                                 log2_chunk=k)
             return [r.hi, r.lo, i.hi, i.lo], st
         from paper_2502_16577_b200.integer import IntProblem
-        words, info = IntProblem(self.m).walk(lo, hi, devices=devices, stats=st)
+        words, info = IntProblem(self.m).walk(lo, hi, devices=devices, stats=st, log2_chunk=k)
         self.even_rows = info.even_rows
         # 192-bit words travel as exact float64 pieces of 32 bits
         return [float((w >> (32 * h)) & 0xFFFFFFFF) for w in words for h in (0, 1)], st

@@ -246,3 +246,13 @@ def test_generated_spa_c128_source_compiles_without_spills(tmp_path, n, exact):
                         "-o", str(tmp_path / "spa.cubin"), str(f)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "0 bytes spill stores" in r.stderr, r.stderr
+
+
+def test_haar_block_is_independent_of_blas_threads():
+    # every rank of a multi-GPU run must rebuild the same matrix whatever
+    # its BLAS thread count (torchrun sets OMP_NUM_THREADS=1 per rank)
+    from threadpoolctl import threadpool_limits
+    a = pk.haar_unitary_block(12, 99).data
+    with threadpool_limits(limits=4):
+        b = pk.haar_unitary_block(12, 99).data
+    assert a == b
