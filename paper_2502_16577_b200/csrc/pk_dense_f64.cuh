@@ -296,24 +296,27 @@ __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0
   constexpr int U = 1 << LOGU;
   DenseWalk<N, C> w(scols);
   const uint64_t base = c << k;
-  const uint64_t rb_mask = rb > 0 ? (1ull << (rb - LOGU)) - 1 : ~0ull;
   if (rb > 0) w.stash_high(x0, base, k, sxs);
   else w.jump_in(x0, base);
   const uint64_t nbody = 1ull << (k - LOGU);
-  for (uint64_t m = 0; m < nbody; ++m) {
-    const uint64_t gb = base + (m << LOGU);
-    if (rb > 0 && (m & rb_mask) == 0) w.rebuild(gb, k, sxs);
-    const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
-    const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
-    StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
-    // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
-    const uint64_t g = gb + U;
-    if (m + 1 < nbody || g <= g_end) {
-      const int j = changed_col(g);
-      w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
-      w.fold(false, false);
+  // segments of bodies between rebuilds: the inner loop is the plain walk
+  const uint64_t seg = rb > 0 && rb - LOGU < k - LOGU ? (1ull << (rb - LOGU)) : nbody;
+  for (uint64_t m0 = 0; m0 < nbody; m0 += seg) {
+    if (rb > 0) w.rebuild(base + (m0 << LOGU), k, sxs);
+    for (uint64_t m = m0; m < m0 + seg; ++m) {
+      const uint64_t gb = base + (m << LOGU);
+      const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
+      const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
+      StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
+      // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
+      const uint64_t g = gb + U;
+      if (m + 1 < nbody || g <= g_end) {
+        const int j = changed_col(g);
+        w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
+        w.fold(false, false);
+      }
+      w.end_body();
     }
-    w.end_body();
   }
   return w.acc.partial();
 }
