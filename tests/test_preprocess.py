@@ -261,3 +261,26 @@ def test_dense_states_match_scalar_state_builders():
         for b in range(4):
             c1, x1 = dense_complex_state(pk.DenseMatrix.from_array(C[b]))
             assert np.array_equal(cols[b], c1) and x0[b].tobytes() == x1.tobytes()
+
+
+def test_native_tree_budgets_and_integer_overflow_fallback():
+    # task budget -> DecompTimeout from the native worklist (no device work)
+    c = case("int20_d30")
+    with pytest.raises(pk.DecompTimeout):
+        pp.decomp_run(pair(c), task_limit=50)
+    # integer folds beyond 128 bits: the native tree declines (None) and
+    # decomp_run falls back to the arbitrary-precision Python worklist
+    n = 8
+    big = 1 << 61
+    trip = [(i, i, big + i) for i in range(n)] + [(i, (i + 1) % n, big - 3 * i) for i in range(n)]
+    trip += [(i, (i + 3) % n, big // 3 + i) for i in range(n)]
+    s = pk.sparse_from_triplets(n, trip, "integer")
+    assert pp._native_tree(s, pp.DEFAULT_TASK_LIMIT, 1e9, 4, pp.DENSE_LEAF_DENSITY) is None
+    leaves, contribs, st = pp.decomp_leaves(s)
+    assert st.tasks_created > 1 and not leaves
+    # exact value by the permutation expansion
+    import itertools
+    rows = pk.sparse_to_dense(s).rows()
+    want = sum(int(np.prod([rows[i][p[i]] for i in range(n)], dtype=object))
+               for p in itertools.permutations(range(n)))
+    assert pp._combine_contributions(contribs, "integer") == want
