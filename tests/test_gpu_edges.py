@@ -149,3 +149,24 @@ def test_reference_error_classes():
     T = pk.total_iterates(12)
     assert pk.run_range(m, T, T).iterations_done == 1
     assert math.isfinite(pk.run_range(m, 1, T).value.hi)
+
+
+def test_concurrent_host_threads_share_a_device_safely():
+    # the C ABI serialises per-device work behind a mutex; ctypes releases the
+    # GIL, so permkit's thread pool can call in concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    ms = [pk.random_real(24, s, 0.0, 1.0) for s in range(6)]
+    want = [pk.perm_nw(m, "kahan") for m in ms]
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        got = list(ex.map(lambda m: pk.perm_nw(m, "kahan"), ms))
+    assert got == want
+    bs = [pk.random_binary(22, s, 0.4) for s in range(4)]
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        got = list(ex.map(pk.permanent, bs))
+    assert got == [pk.permanent(b) for b in bs]
+
+
+def test_missing_device_ordinal_is_a_device_error():
+    m = pk.random_real(14, 2)
+    with pytest.raises(pk.DeviceError):
+        pk.perm_nw(m, "kahan", devices=[pk._native.device_count() + 3])
