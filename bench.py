@@ -326,19 +326,21 @@ class Workload:
         chunks for real / integer walks, 2^19 for complex; pk_abi.cu
         plan_dense). Every rank uses it, so an N-rank split walks exactly the
         single-GPU chunks and reproduces its bits (power-of-two N)."""
-        from paper_2502_16577_b200.csrc_params import c128_logu, dense_logu
+        from paper_2502_16577_b200.csrc_params import auto_log2_chunk, c128_logu, dense_logu
         n = self.n
         if self.kind == "haar":
-            return max(c128_logu(n) + 1, (n - 1) - 19)
+            return auto_log2_chunk(n - 1, c128_logu(n), 19)
         logu = 2 if self.kind == "binary" else dense_logu(n)
-        return max(logu + 1, (n - 1) - 22)
+        return auto_log2_chunk(n - 1, logu, 22)
 
     def walk(self, lo, hi, devices):
         """(partial as a list of floats for the gather, stats)"""
         from paper_2502_16577_b200 import _native
         from paper_2502_16577_b200.precision import AccumulatorPolicy
         st = _native.RunStats()
-        k = self.whole_walk_log2_chunk()
+        # whole walks: the single-GPU chunking on every rank (bit-identical
+        # splits); --range-log2 samples: the library's own choice for the range
+        k = 0 if self.range_sample else self.whole_walk_log2_chunk()
         if self.kind == "dense":
             from paper_2502_16577_b200.kernels import DenseF64Problem
             p = DenseF64Problem(self.m).walk(lo, hi, AccumulatorPolicy.parse(self.policy),
@@ -451,6 +453,7 @@ def run_b200(args, dist: Dist):
     from paper_2502_16577_b200 import _native
 
     wl = Workload(args)
+    wl.range_sample = bool(args.range_log2)
     n, N, rank = wl.n, dist.world, dist.rank
     total = (1 << (n - 1)) - 1
     if args.range_log2:

@@ -6,6 +6,7 @@
 // whole range: its aligned middle goes to the N-specialised register kernels
 // (one tree-reduced double-double per device), the unaligned head and tail
 // to the range walkers; the host combines the pieces in a fixed order.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -216,7 +217,13 @@ DensePlan plan_dense(int n, int logu, uint64_t start, uint64_t end, int log2_chu
   if (logu > 0) {
     int k = log2_chunk;
     if (k <= 0) {
-      k = bit_length(len) - chunks_log2;
+      // ~2^chunks_log2 chunks for long walks; mid-size walks keep chunks of
+      // at least 2^8 steps (while 2^17 chunks remain) so the per-chunk
+      // jump-in and reduction stay small against the walk
+      const int bl = bit_length(len);
+      k = bl - chunks_log2;
+      const int k_floor = std::min(8, bl - 17);
+      if (k < k_floor) k = k_floor;
       if (k < logu + 1) k = logu + 1;
     }
     if (k < logu + 1 || k > n - 1 - 5)

@@ -16,3 +16,10 @@ def batch_log2_chunk(n: int, logu: int) -> int:
 
 def c128_logu(n: int) -> int:
     return 2 if n <= 32 else 1
+
+
+def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:
+    """pk_abi.cu plan_dense's automatic chunk exponent for a range whose
+    length has `bit_len` bits (a whole walk: n - 1)."""
+    k = max(bit_len - chunks_log2, min(8, bit_len - 17))
+    return max(k, logu + 1)
