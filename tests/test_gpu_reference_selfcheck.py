@@ -74,3 +74,34 @@ def test_reference_selfcheck_passes_on_the_gpu_backend(permkit_ref, monkeypatch,
     assert ok, out
     assert "FAIL" not in out
     assert calls["perm"] > 100 and calls["range"] > 10, calls
+
+
+@pytest.mark.parametrize("kind", ["real64", "integer", "complex128"])
+def test_reference_merges_our_gpu_partial_files(permkit_ref, tmp_path, kind):
+    # each GPU (here: each process index of a hierarchy
+    # plan) emits the reference's partial-file format; permkit's own
+    # merge_partial_files reads them and reduces to our value
+    import permkit.generate as rg
+    import permkit.parallel as rp
+    from permkit.matrix import DenseMatrix as RefDense
+    n = 14
+    if kind == "real64":
+        ours = pk.random_real(n, 5, 0.0, 1.0)
+    elif kind == "integer":
+        ours = pk.random_binary(n, 5, 0.5)
+    else:
+        ours = pk.haar_unitary_block(n, 5)
+    ref_m = RefDense.from_rows(ours.rows())
+    hp = pk.plan_hierarchy(n, 4, 2)
+    paths = []
+    for pi in range(hp.processes):
+        parts = pk.execute_hierarchy(ours, hp, "dd", process_index=pi)
+        path = tmp_path / f"partial-{pi}.txt"
+        pk.write_partials_file(path, ours, "dd", parts)
+        paths.append(str(path))
+    ref_val = rp.merge_partial_files(paths, ref_m, rp.AccumulatorPolicy.DD)
+    our_val = pk.merge_partial_files(paths, ours, "dd")
+    assert ref_val == our_val
+    single = pk.reduce_partials(pk.execute_hierarchy(ours, hp, "dd"),
+                                pk.initial_product(ours, "dd"), n)
+    assert ref_val == single
