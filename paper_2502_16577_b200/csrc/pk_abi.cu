@@ -218,11 +218,12 @@ DensePlan plan_dense(int n, int logu, uint64_t start, uint64_t end, int log2_chu
     int k = log2_chunk;
     if (k <= 0) {
       // ~2^chunks_log2 chunks for long walks; mid-size walks keep chunks of
-      // at least 2^8 steps (while 2^17 chunks remain) so the per-chunk
-      // jump-in and reduction stay small against the walk
+      // up to 2^12 steps (while 2^17 chunks remain) so the per-chunk jump-in
+      // and reduction stay small against the walk
+      // (profiles/r01_k1_variants_sweep8_n32.txt, r01_k1_sweep_n.md)
       const int bl = bit_length(len);
       k = bl - chunks_log2;
-      const int k_floor = std::min(8, bl - 17);
+      const int k_floor = std::min(12, bl - 17);
       if (k < k_floor) k = k_floor;
       if (k < logu + 1) k = logu + 1;
     }

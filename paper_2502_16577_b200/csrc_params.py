@@ -21,5 +21,5 @@ def c128_logu(n: int) -> int:
 def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:
     """pk_abi.cu plan_dense's automatic chunk exponent for a range whose
     length has `bit_len` bits (a whole walk: n - 1)."""
-    k = max(bit_len - chunks_log2, min(8, bit_len - 17))
+    k = max(bit_len - chunks_log2, min(12, bit_len - 17))
     return max(k, logu + 1)
