@@ -150,6 +150,9 @@ DevCtx& dev_ctx(int d) {
   return c;
 }
 
+// dd_t workspace slots that hold `count` i192 values (24 B each)
+size_t i192_slots(size_t count) { return (count * 3 + 1) / 2; }
+
 template <class T>
 void ensure(T*& p, size_t& cap, size_t need) {
   if (need <= cap) return;
@@ -903,7 +906,7 @@ void run_int_on_device(int dev, const IntPrep& ip, const DensePlan& pl, uint64_t
     ck(cudaEventRecord(c.e0, c.stream), "event record");
     // i192 buffers are carved from the dd workspaces (24 B <= 32 B per dd pair)
     if (g_cnt > 0 && ip.sparse) {
-      ensure(c.groups, c.groups_cap, g_cnt);
+      ensure(c.groups, c.groups_cap, i192_slots(g_cnt));
       pk::SpaIntSpec sp;
       sp.n = ip.n;
       sp.zcols = ip.zcols;
@@ -925,7 +928,7 @@ void run_int_on_device(int dev, const IntPrep& ip, const DensePlan& pl, uint64_t
       if (rc != 0) fail(PK_ERR_CUDA, err);
       ++r.launches;
     } else if (g_cnt > 0) {
-      ensure(c.groups, c.groups_cap, g_cnt);
+      ensure(c.groups, c.groups_cap, i192_slots(g_cnt));
       pk::IntLaunch a{};
       a.d_cols = d_cols;
       a.z0 = ip.z0.data();
@@ -944,7 +947,7 @@ void run_int_on_device(int dev, const IntPrep& ip, const DensePlan& pl, uint64_t
       ++r.launches;
     }
     if (!pieces.empty()) {
-      ensure(c.chunks, c.chunks_cap, pieces.size());
+      ensure(c.chunks, c.chunks_cap, i192_slots(pieces.size()));
       launch_walk_int(c, ip, d_cols, d_z0, d_s, d_e, (int)pieces.size(), (pk::i192*)c.chunks);
       ++r.launches;
     }
@@ -1187,7 +1190,7 @@ int pk_int_ranges(const int64_t* a, int n, const uint64_t* starts, const uint64_
     const unsigned long long *d_s, *d_e;
     const int* d_z0;
     const int* d_cols = upload_int(c, ip, rs, &d_s, &d_e, &d_z0);
-    ensure(c.chunks, c.chunks_cap, rs.size());
+    ensure(c.chunks, c.chunks_cap, i192_slots(rs.size()));
     launch_walk_int(c, ip, d_cols, d_z0, d_s, d_e, nranges, (pk::i192*)c.chunks);
     ck(cudaStreamSynchronize(c.stream), "walker execution");
     ck(cudaMemcpy(out_z, c.chunks, rs.size() * sizeof(pk::i192), cudaMemcpyDeviceToHost), "D2H");
@@ -1478,13 +1481,13 @@ int pk_int_batch(const int64_t* a, int n, int batch, int device, uint64_t* out_z
     if (nc) ck(cudaMemcpyAsync(d_cols, hcols.data(), nc * batch * 4, cudaMemcpyHostToDevice, c.stream), "H2D cols");
     ck(cudaMemcpyAsync(d_z0, hz0.data(), (size_t)n * batch * 4, cudaMemcpyHostToDevice, c.stream), "H2D z0");
     // i192 outputs in the dd workspaces (24 B <= 32 B per dd pair)
-    ensure(c.chunks, c.chunks_cap, (size_t)batch);
+    ensure(c.chunks, c.chunks_cap, i192_slots((size_t)batch));
     ck(cudaEventRecord(c.e0, c.stream), "event record");
     int k = 0;
     if (n >= pk::kIntNMin) {
       k = pk::batch_log2_chunk(n, pk::int_logu(n));
       const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
-      ensure(c.groups, c.groups_cap, groups * batch);
+      ensure(c.groups, c.groups_cap, i192_slots(groups * batch));
       pk::IntBatchLaunch l{};
       l.d_cols = d_cols;
       l.d_z0 = d_z0;
