@@ -1,0 +1,29 @@
+"""Small calls through every device path, for compute-sanitizer memcheck."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2502_16577_b200 as pk  # noqa: E402
+from paper_2502_16577_b200.integer import IntProblem, int_batch_totals  # noqa: E402
+
+m = pk.random_real(22, 3, 0.0, 1.0)
+print(pk.perm_nw(m, "kahan"), pk.perm_nw(m, "qq"), pk.run_range(m, 3, 70001, "dq").value)
+print(pk.perm_nw(pk.random_real(9, 1)))
+s = pk.random_sparse_real(20, 0.4, 7, 0.0, 1.0)
+print(pk.perm_spa(s, "kahan"))
+h = pk.haar_unitary_block(18, 2)
+print(pk.perm_nw(h), pk.perm_spa(pk.dense_to_sparse(h)))
+b = pk.random_binary(24, 5, 0.4)
+print(pk.permanent(b), pk.perm_spa(pk.dense_to_sparse(b)))
+prob = IntProblem(b)
+T = pk.total_iterates(24)
+print(pk.run_range(b, 5, T - 7).value)
+print(prob.ranges([(1, 1000), (5000, 90000)])[0][0])
+print(int_batch_totals([pk.random_binary(16, k, 0.5) for k in range(5)]))
+print(int_batch_totals([pk.random_binary(8, k, 0.5) for k in range(5)]))
+print(pk.permanent_batch([pk.random_real(14, k) for k in range(4)] + [pk.haar_unitary_block(12, 1)]))
+big = pk.random_binary(38, 9, 0.3)
+print(IntProblem(big).walk(1, 1 << 24)[0])
+print(pk.decomp_run(pk.random_sparse_real(16, 0.35, 3, 0.0, 1.0), "kahan")[0])
+print("memcheck paths done")
