@@ -1,0 +1,15 @@
+"""A few small launches of each kernel family for compute-sanitizer racecheck."""
+import sys
+
+sys.path.insert(0, ".")
+import paper_2502_16577_b200 as pk  # noqa: E402
+from paper_2502_16577_b200.integer import int_batch_totals  # noqa: E402
+
+print(pk.perm_nw(pk.random_real(16, 3, 0.0, 1.0), "kahan"))
+print(pk.perm_nw(pk.haar_unitary_block(14, 2)))
+print(pk.permanent(pk.random_binary(16, 5, 0.4)))
+print(pk.permanent_batch([pk.random_real(13, k) for k in range(3)]))
+print(pk.permanent_batch([pk.haar_unitary_block(12, k) for k in range(3)]))
+print(int_batch_totals([pk.random_binary(13, k, 0.5) for k in range(3)]))
+print(pk.perm_spa(pk.random_sparse_real(16, 0.4, 7, 0.0, 1.0), "kahan"))
+print("racecheck paths done")
