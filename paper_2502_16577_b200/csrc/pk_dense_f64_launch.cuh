@@ -39,6 +39,7 @@ int launch_dense_f64(const DenseLaunch& a) {
   static_assert(N >= kDenseNMin && N <= kDenseNMax, "order out of range");
   constexpr int LOGU = dense_logu(N);
   constexpr int MB = dense_minb(N);
+  constexpr int BLK = dense_block(N), BMB = dense_block_minb(N);
   DenseF64Params<N> p;
   std::memcpy(p.cols, a.cols, sizeof(double) * (N - 1) * N);
   std::memcpy(p.x0, a.x0, sizeof(double) * N);
@@ -54,13 +55,13 @@ int launch_dense_f64(const DenseLaunch& a) {
   switch (a.policy) {
     case POL_DD:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, MB, 128, true>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_KAHAN:
       return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, MB, 128, true>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_DQ:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, MB, 128, true>>(a, p);
+                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_QQ:
       return a.exact ? launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true>>(a, p);

@@ -17,6 +17,11 @@ constexpr int kDenseNMax = 63;
 // resident 128-thread blocks per SM up to N = 36, two above.
 constexpr int dense_logu(int N) { return N <= 50 ? 4 : 3; }
 constexpr int dense_minb(int N) { return N <= 36 ? 3 : 2; }
+// fast-mode block shape of the chunk kernel: one large block per SM beats
+// several 128-thread blocks with the same warp count by 4-6 % from n = 33
+// (profiles/r01_k1_variants_sweep10_blocks.txt); n <= 32 keeps 3 x 128
+constexpr int dense_block(int N) { return N <= 32 ? 128 : (N <= 36 ? 384 : 256); }
+constexpr int dense_block_minb(int N) { return N <= 32 ? 3 : 1; }
 // fast QQ (DenseCfg::QF) carries two registers per product chain: shorter
 // bodies (profiles/r01_qf_sweep.txt)
 constexpr int qf_logu(int N) { return N <= 36 ? 2 : 3; }
