@@ -40,9 +40,9 @@ struct DenseC128Params {
 // FA (fast mode): the last complex multiply of each product and the body sum
 // fold into four DFMAs, b += (+-p) * x[N-1] per component (two FP64
 // instructions fewer per update)
-template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false>
+template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false, int BLOCK_ = kC128Block>
 struct C128Cfg {
-  static constexpr int LOGU = LOGU_, MINB = MINB_;
+  static constexpr int LOGU = LOGU_, MINB = MINB_, BLOCK = BLOCK_;
   static constexpr bool EXACT = EXACT_;
   static constexpr bool FA = FA_ && !EXACT_;
 };
@@ -263,7 +263,7 @@ __device__ __forceinline__ void warp_tree_cdd(dd_t& re, dd_t& im) {
 }
 
 template <int N, class C>
-__global__ void __launch_bounds__(kC128Block, C::MINB)
+__global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_c128_chunks(const __grid_constant__ DenseC128Params<N> p) {
   extern __shared__ __align__(16) double scols[];
   for (int t = threadIdx.x; t < 2 * (N - 1) * N; t += blockDim.x) scols[t] = p.cols[t];
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kC128Block, C::MINB)
       p.group_part[2 * grp + 1] = im;
     }
   }
-  grid_tail_reduce_pairs<kC128Block>(p.group_part, p.num_groups, p.out, p.counter);
+  grid_tail_reduce_pairs<C::BLOCK>(p.group_part, p.num_groups, p.out, p.counter);
 }
 
 template <int N>

@@ -19,15 +19,15 @@ static int launch_c128_cfg(const C128Launch& a, const DenseC128Params<N>& p) {
       if (e != cudaSuccess) return (int)e;
     }
     int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kC128Block, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
     if (e != cudaSuccess) return (int)e;
     occ = o > 0 ? o : 1;
   }
-  const uint64_t blocks_needed = (a.num_groups * 32 + kC128Block - 1) / kC128Block;
+  const uint64_t blocks_needed = (a.num_groups * 32 + C::BLOCK - 1) / C::BLOCK;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kC128Block, smem, a.stream>>>(p);
+  kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);
   return (int)cudaGetLastError();
 }
 
@@ -47,8 +47,14 @@ int launch_dense_c128(const C128Launch& a) {
   p.num_groups = a.num_groups;
   p.g_end = a.g_end;
   p.k = a.k;
-  return a.exact ? launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p)
-                 : launch_c128_cfg<N, C128Cfg<LOGU, false, MB>>(a, p);
+  // fast mode: one 256-thread block per SM to n = 32 (+5 %,
+  // profiles/r01_c128_sweep5_blocks.txt); results do not depend on it
+  if constexpr (N <= 32)
+    return a.exact ? launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p)
+                   : launch_c128_cfg<N, C128Cfg<LOGU, false, 1, false, 256>>(a, p);
+  else
+    return a.exact ? launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p)
+                   : launch_c128_cfg<N, C128Cfg<LOGU, false, MB>>(a, p);
 }
 
 template <int N, class C>
