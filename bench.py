@@ -256,7 +256,9 @@ def run_reference(args, dist: Dist):
     args.n = args.n or 40
     rows = matrix_rows(args.n)
     samples = []
-    log2 = min(args.cpu_sample_log2 - 2, args.n - 2)
+    # >= 2^31 iterates per step (about 2.5 s of numba work on 16 cores), so
+    # thread start-up and the JIT's first-call costs do not depress the rate
+    log2 = min(args.cpu_sample_log2, args.n - 2)
     for i in range(args.warmup + args.steps):
         r = cpu_updates_per_s(args.n, args.policy, log2, rows)
         if i >= args.warmup:

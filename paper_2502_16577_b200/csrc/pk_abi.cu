@@ -373,11 +373,15 @@ int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
 }
 
 // state rebuild period of the fast real walks (pk_launch.h); the
-// PK_REBUILD_LOG2 environment variable overrides it (0 = off) for A/B runs
+// PK_REBUILD_LOG2 environment variable overrides it (0 = off) for A/B runs.
+// A period must cover whole bodies (>= the longest body, 2^4 steps); other
+// values are ignored.
 int rebuild_log2() {
   static const int v = [] {
     const char* e = getenv("PK_REBUILD_LOG2");
-    return e ? atoi(e) : pk::kDenseRebuildLog2;
+    if (!e) return pk::kDenseRebuildLog2;
+    const int r = atoi(e);
+    return (r == 0 || (r >= 4 && r <= 62)) ? r : pk::kDenseRebuildLog2;
   }();
   return v;
 }

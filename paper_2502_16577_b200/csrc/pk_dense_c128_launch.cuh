@@ -11,18 +11,9 @@ template <int N, class C>
 static int launch_c128_cfg(const C128Launch& a, const DenseC128Params<N>& p) {
   auto kern = dense_c128_chunks<N, C>;
   constexpr size_t smem = c128_smem_bytes<N>();
-  static int occ = -1;
-  if (occ < 0) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return (int)e;
-    }
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
   const uint64_t blocks_needed = (a.num_groups * 32 + C::BLOCK - 1) / C::BLOCK;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if (blocks_needed < grid) grid = blocks_needed;
@@ -48,7 +39,8 @@ int launch_dense_c128(const C128Launch& a) {
   p.g_end = a.g_end;
   p.k = a.k;
   // fast mode: one 256-thread block per SM to n = 32 (+5 %,
-  // profiles/r01_c128_sweep5_blocks.txt); results do not depend on it
+  // profiles/r01_c128_sweep5_blocks.txt); the tail tree has a fixed leaf
+  // count (pk_reduce.cuh kTreeLeaves), so results do not depend on it
   if constexpr (N <= 32)
     return a.exact ? launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p)
                    : launch_c128_cfg<N, C128Cfg<LOGU, false, 1, false, 256>>(a, p);
@@ -61,18 +53,9 @@ template <int N, class C>
 static int launch_c128_batch_cfg(const C128BatchLaunch& a) {
   auto kern = dense_c128_batch<N, C>;
   constexpr size_t smem = c128_smem_bytes<N>() + sizeof(double) * 2 * N;
-  static int occ = -1;
-  if (occ < 0) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return (int)e;
-    }
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kC128Block, smem);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, kC128Block, smem, slots, &occ)) return rc;
   C128BatchParams<N> p;
   p.cols = a.d_cols;
   p.x0 = a.d_x0;

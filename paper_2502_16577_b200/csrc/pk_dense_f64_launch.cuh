@@ -13,18 +13,9 @@ static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
   auto kern = dense_f64_chunks<N, C>;
   // columns + the per-thread rebuild stash (fast modes)
   constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * C::BLOCK;
-  static int occ = -1;  // per instantiation; every B200 gives the same answer
-  if (occ < 0) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return (int)e;
-    }
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
   const uint64_t warps_needed = a.num_groups;
   const uint64_t blocks_needed = (warps_needed * 32 + C::BLOCK - 1) / C::BLOCK;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
@@ -74,18 +65,9 @@ template <int N, class C>
 static int launch_batch_cfg(const DenseBatchLaunch& a) {
   auto kern = dense_f64_batch<N, C>;
   constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * (1 + C::BLOCK);
-  static int occ = -1;
-  if (occ < 0) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return (int)e;
-    }
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::BLOCK, smem);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
   DenseBatchParams<N> p;
   p.cols = a.d_cols;
   p.x0 = a.d_x0;

@@ -10,13 +10,9 @@ namespace pk {
 template <int N, class C>
 static int launch_int_cfg(const IntLaunch& a, const IntParams<N>& p) {
   auto kern = int_chunks<N, C>;
-  static int occ = -1;
-  if (occ < 0) {
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kIntBlock, 0);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, kIntBlock, 0, slots, &occ)) return rc;
   const uint64_t blocks_needed = (a.num_groups * 32 + kIntBlock - 1) / kIntBlock;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if (blocks_needed < grid) grid = blocks_needed;
@@ -53,13 +49,9 @@ int launch_int(const IntLaunch& a) {
 template <int N, class C>
 static int launch_int_batch_cfg(const IntBatchLaunch& a) {
   auto kern = int_batch<N, C>;
-  static int occ = -1;
-  if (occ < 0) {
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kIntBlock, 0);
-    if (e != cudaSuccess) return (int)e;
-    occ = o > 0 ? o : 1;
-  }
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, kIntBlock, 0, slots, &occ)) return rc;
   IntBatchParams<N> p;
   p.cols = a.d_cols;
   p.z0 = a.d_z0;

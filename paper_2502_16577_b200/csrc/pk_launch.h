@@ -2,11 +2,42 @@
 // per-N kernel instantiation units (pk_dense_f64_n*.cu).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 #include "pk_common.cuh"
 
 namespace pk {
+
+constexpr int kMaxDevices = 64;
+
+// Per-device launch preparation of one kernel instantiation: function
+// attributes (the dynamic shared-memory opt-in above 48 KB) are per device,
+// so they are set -- and the occupancy measured -- once for every device
+// ordinal the kernel is launched on. `slots` is the instantiation's own
+// table (a function-local static of the caller); concurrent host threads of
+// different devices touch different slots, and a race on one slot only
+// repeats the idempotent attribute call.
+template <class K>
+inline int prep_kernel(K kern, int block, size_t smem, std::atomic<int>* slots, int* occ) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  if (dev < 0 || dev >= kMaxDevices) return (int)cudaErrorInvalidDevice;
+  int o = slots[dev].load(std::memory_order_acquire);
+  if (o <= 0) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, block, smem);
+    if (e != cudaSuccess) return (int)e;
+    if (o < 1) o = 1;
+    slots[dev].store(o, std::memory_order_release);
+  }
+  *occ = o;
+  return 0;
+}
 
 constexpr int kDenseNMin = 11;  // below this the range walkers take the whole walk
 constexpr int kDenseNMax = 63;

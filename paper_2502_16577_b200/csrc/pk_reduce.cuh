@@ -38,14 +38,21 @@ __device__ inline dd_t pairwise_fold(const dd_t* parts, uint64_t lo, uint64_t hi
   return acc;
 }
 
+// Leaf count of the tail tree. It is a constant of the library, not of the
+// launching kernel: every kernel -- dense or sparse, fast or exact, whatever
+// its block size -- folds the same group partials in the same order, so the
+// sparse and dense walks of one matrix agree bit for bit for any group count.
+constexpr unsigned int kTreeLeaves = 128;
+
 // Called by every block at the end of a chunk kernel. The last block to
 // arrive folds the S interleaved streams of group partials (parts[i*S + s])
 // into out[s] and re-arms the counter.
 template <int BLOCK, int S>
 __device__ inline void grid_tail_reduce_streams(const dd_t* parts, uint64_t count, dd_t* out,
                                                 unsigned int* counter) {
+  static_assert(BLOCK >= (int)kTreeLeaves, "the tail tree needs kTreeLeaves threads");
   __shared__ bool is_last;
-  __shared__ dd_t tree[BLOCK];
+  __shared__ dd_t tree[kTreeLeaves];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -56,7 +63,7 @@ __device__ inline void grid_tail_reduce_streams(const dd_t* parts, uint64_t coun
   if (!is_last) return;
   __threadfence();
   unsigned int b = 1;
-  while (2ull * b <= (uint64_t)BLOCK && 2ull * b <= count) b *= 2;
+  while (2ull * b <= (uint64_t)kTreeLeaves && 2ull * b <= count) b *= 2;
   const unsigned int t = threadIdx.x;
   for (int s = 0; s < S; ++s) {
     if (t < b && count > 0) {

@@ -63,12 +63,14 @@ def permanent_distributed(matrix, policy="kahan", *, group=None, device: Optiona
     policy = as_policy(policy)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    # this rank's GPU: the one the walk runs on is also where NCCL gathers
+    dev_idx = device if device is not None else int(os.environ.get("LOCAL_RANK", 0))
     if walker is None:
-        walker = _gpu_walker(device if device is not None else int(os.environ.get("LOCAL_RANK", 0)))
+        walker = _gpu_walker(dev_idx)
     lo, hi = rank_span(m.n, rank, world)
     part = walker(m, policy, lo, hi) if lo <= hi else (0.0, 0.0)
     backend = dist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    dev = torch.device("cuda", dev_idx) if backend == "nccl" else "cpu"
     t = torch.tensor(list(part), dtype=torch.float64, device=dev)
     got = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(got, t, group=group)
