@@ -32,6 +32,7 @@ PK_ERR_OVERFLOW = 6
 
 PK_FLAG_EXACT = 1
 PK_FLAG_SPARSE = 2
+PK_FLAG_PRECISE = 4
 
 
 class RunStats(ctypes.Structure):

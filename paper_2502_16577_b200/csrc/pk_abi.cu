@@ -7,6 +7,7 @@
 // (one tree-reduced double-double per device), the unaligned head and tail
 // to the range walkers; the host combines the pieces in a fixed order.
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -372,29 +373,87 @@ int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
   }
 }
 
-// state rebuild period of the fast real walks (pk_launch.h); the
-// PK_REBUILD_LOG2 environment variable overrides it (0 = off) for A/B runs.
-// A period must cover whole bodies (>= the longest body, 2^4 steps); other
-// values are ignored.
-int rebuild_log2() {
-  static const int v = [] {
-    const char* e = getenv("PK_REBUILD_LOG2");
-    if (!e) return pk::kDenseRebuildLog2;
-    const int r = atoi(e);
-    return (r == 0 || (r >= 4 && r <= 62)) ? r : pk::kDenseRebuildLog2;
-  }();
-  return v;
-}
-
 size_t ncols_of(int n) { return (size_t)(n > 1 ? n - 1 : 1) * n; }
 
+// Exact walk states for the fast modes (DESIGN.md §5 "x state"). The
+// reference updates the row sums x_i incrementally in double, and every
+// update rounds; the drift is what limits its accuracy (1.2e-9 at n = 36
+// with 2^19-step chunks, tests/test_gpu_configs.py). Here the fast kernels
+// walk the input rounded once onto a per-row (and per component) fixed-point
+// grid 2^-F: with B = |x0_i| + sum_j |a_ij| < 2^e and F = 52 - e, every
+// subset sum x0_i + sum_{j in S} a_ij of grid values is a multiple of 2^-F
+// below 2^(e+1) in magnitude, i.e. a double -- so the jump-in sums and every
+// update are exact and the states never drift. The rounding moves each entry
+// by at most 2^-(F+1) <= B 2^-53 (half an ulp of the row's largest possible
+// state), once, instead of a rounding of that size at every step.
+// comps = 1 (real) or 2 (complex, interleaved re/im: independent grids).
+void quantize_walk(const double* cols, const double* x0, int n, int comps, double* qcols,
+                   double* qx0) {
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < comps; ++c) {
+      double bound = std::fabs(x0[(size_t)comps * i + c]);
+      for (int j = 0; j < n - 1; ++j) bound += std::fabs(cols[(size_t)comps * (j * n + i) + c]);
+      int F = 0;
+      const bool grid = bound > 0.0 && std::isfinite(bound);
+      if (grid) {
+        int e = 0;
+        std::frexp(bound, &e);  // bound < 2^e
+        F = 52 - e;
+      }
+      auto q = [&](double v) { return grid ? std::ldexp(std::nearbyint(std::ldexp(v, F)), -F) : v; };
+      qx0[(size_t)comps * i + c] = q(x0[(size_t)comps * i + c]);
+      for (int j = 0; j < n - 1; ++j)
+        qcols[(size_t)comps * (j * n + i) + c] = q(cols[(size_t)comps * (j * n + i) + c]);
+    }
+}
+
+// Fixed-point image of a dense real walk for the precise mode (pk_precise.cuh).
+// Row i gets a scale 2^F_i with (|x0_i| + sum_j |a_ij|) 2^F_i < 2^62, so
+// X_i = x0_i 2^F_i + sum_{j in S} a_ij 2^F_i is an exact int64 for every
+// column subset S; every entry is rounded to the row's grid once (RN,
+// |error| <= 2^-(F_i+1), 2^-63 of the row's absolute sum). Layout (int64
+// words): A[j*n + i] for the n-1 walked columns, X0[n], then the bit
+// patterns of the doubles 2^-F_i[n].
+size_t fix_words_of(int n) { return (size_t)(n > 1 ? n - 1 : 0) * n + 2 * (size_t)n; }
+
+void fixed_image(const double* cols, const double* x0, int n, long long* out) {
+  long long* A = out;
+  long long* X0 = out + (size_t)(n - 1) * n;
+  long long* sc = X0 + n;
+  for (int i = 0; i < n; ++i) {
+    double bound = std::fabs(x0[i]);
+    for (int j = 0; j < n - 1; ++j) bound += std::fabs(cols[(size_t)j * n + i]);
+    int F = 0;
+    if (bound > 0.0 && std::isfinite(bound)) {
+      int e = 0;
+      std::frexp(bound * (1.0 + 0x1p-40), &e);  // bound (with slack) < 2^e
+      F = 62 - e;
+      if (F > 1000) F = 1000;    // 2^-F stays a normal double
+      if (F < -1000) F = -1000;
+    }
+    for (int j = 0; j < n - 1; ++j)
+      A[(size_t)j * n + i] = std::llrint(std::ldexp(cols[(size_t)j * n + i], F));
+    X0[i] = std::llrint(std::ldexp(x0[i], F));
+    const double s = std::ldexp(1.0, -F);
+    std::memcpy(&sc[i], &s, 8);
+  }
+}
+
 Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, bool exact,
-                    bool sparse = false) {
+                    bool sparse = false, bool precise = false) {
   Kind kd;
   kd.n = n;
   kd.streams = 1;
   kd.logu = n >= pk::kDenseNMin ? pk::dense_logu(n) : 0;
   const size_t nc = ncols_of(n);
+  // fast modes walk the input rounded onto the per-row grids (exact states)
+  std::shared_ptr<std::vector<double>> qbuf;
+  if (!exact && !precise && n >= pk::kDenseNMin) {
+    qbuf = std::make_shared<std::vector<double>>(nc + n);
+    quantize_walk(cols, x0, n, 1, qbuf->data(), qbuf->data() + nc);
+    cols = qbuf->data();
+    x0 = qbuf->data() + nc;
+  }
   kd.input.assign(nc + n, 0.0);
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 8);
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 8);
@@ -422,7 +481,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                   uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
       pk::SpaF64Launch a{};
-      a.rb = rebuild_log2();
+      a.rb = 0;  // exact states: nothing to rebuild
       a.d_cols = d_in;
       a.d_x0 = d_in + nc;
       a.d_vals = d_in + voff;
@@ -441,16 +500,37 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
       if (rc != 0) fail(PK_ERR_CUDA, err);
       return 0;
     };
+  } else if (precise && n >= pk::kDenseNMin) {
+    // precise mode: exact fixed-point state, double-double products and sums
+    const size_t fo = kd.input.size();
+    kd.input.resize(fo + fix_words_of(n), 0.0);
+    fixed_image(cols, x0, n, reinterpret_cast<long long*>(kd.input.data() + fo));
+    kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                  uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+      pk::PreciseLaunch a{};
+      a.fix = reinterpret_cast<const long long*>(d_in + fo);
+      a.k = k;
+      a.chunk_lo = chunk_lo;
+      a.num_groups = groups;
+      a.g_end = g_end;
+      a.group_part = gparts;
+      a.chunk_part = cparts;
+      a.out = out;
+      a.counter = c.counter;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      return pk::launch_dense_f64_precise(n, a);
+    };
   } else {
   kd.fast = [=](DevCtx& c, const double*, uint64_t chunk_lo, uint64_t groups, uint64_t g_end,
                 int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+    (void)qbuf;  // keeps the quantized inputs alive with the lambda
     pk::DenseLaunch a{};
     a.cols = h_cols;
     a.x0 = h_x0;
     a.policy = policy;
     a.exact = exact;
     a.k = k;
-    a.rb = rebuild_log2();
     a.chunk_lo = chunk_lo;
     a.num_groups = groups;
     a.g_end = g_end;
@@ -508,6 +588,14 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   kd.logu = (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
   kd.chunks_log2 = 19;
   const size_t nc = 2 * ncols_of(n);
+  // fast modes walk the input rounded onto per-row, per-component grids
+  std::shared_ptr<std::vector<double>> qbuf;
+  if (!exact && kd.logu > 0) {
+    qbuf = std::make_shared<std::vector<double>>(nc + 2 * n);
+    quantize_walk(cols, x0, n, 2, qbuf->data(), qbuf->data() + nc);
+    cols = qbuf->data();
+    x0 = qbuf->data() + nc;
+  }
   kd.input.assign(nc + 2 * n, 0.0);
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 16);
@@ -546,6 +634,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   } else {
   kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                 uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+    (void)qbuf;  // keeps the rounded inputs alive with the lambda
     pk::C128Launch a{};
     a.d_cols = d_in;
     a.x0 = h_x0;
@@ -1033,7 +1122,7 @@ int pk_dense_f64(const double* cols, const double* x0, int n, uint64_t start, ui
     if (!x0 || !out_dd || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
     Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0,
-                             (flags & PK_FLAG_SPARSE) != 0);
+                             (flags & PK_FLAG_SPARSE) != 0, (flags & PK_FLAG_PRECISE) != 0);
     dd_t out[2];
     drive(kd, start, end, log2_chunk, device_list(devices, ndev), out, stats);
     out_dd[0] = out[0].hi;
@@ -1063,7 +1152,7 @@ int pk_dense_f64_chunks(const double* cols, const double* x0, int n, int log2_ch
     check_policy(policy);
     if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
     Kind kd = dense_f64_kind(cols, x0, n, policy, (flags & PK_FLAG_EXACT) != 0,
-                             (flags & PK_FLAG_SPARSE) != 0);
+                             (flags & PK_FLAG_SPARSE) != 0, (flags & PK_FLAG_PRECISE) != 0);
     dd_t tot[2];
     drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
     out_total[0] = tot[0].hi;
@@ -1214,6 +1303,17 @@ int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, i
     DevCtx& c = dev_ctx(device);
     std::lock_guard<std::mutex> lock(c.mu);
     ck(cudaSetDevice(device), "cudaSetDevice");
+    // fast modes: every matrix rounded onto its per-row grids (exact states)
+    std::vector<double> qcols, qx0;
+    if ((flags & PK_FLAG_EXACT) == 0 && n >= pk::kDenseNMin) {
+      qcols.resize(ncol * batch);
+      qx0.resize((size_t)n * batch);
+      for (int b = 0; b < batch; ++b)
+        quantize_walk(cols + (size_t)b * ncol, x0 + (size_t)b * n, n, 1,
+                      qcols.data() + (size_t)b * ncol, qx0.data() + (size_t)b * n);
+      cols = qcols.data();
+      x0 = qx0.data();
+    }
     const size_t in_doubles = ncol * batch + (size_t)n * batch;
     ensure(c.scratch, c.scratch_cap, in_doubles * 8 + 64);
     double* d_cols = (double*)c.scratch;
@@ -1234,7 +1334,6 @@ int pk_dense_f64_batch(const double* cols, const double* x0, int n, int batch, i
       a.exact = (flags & PK_FLAG_EXACT) != 0;
       a.batch = batch;
       a.k = k;
-      a.rb = rebuild_log2();
       a.group_part = c.groups;
       a.out = c.chunks;
       a.stream = c.stream;
@@ -1381,6 +1480,17 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
     DevCtx& c = dev_ctx(device);
     std::lock_guard<std::mutex> lock(c.mu);
     ck(cudaSetDevice(device), "cudaSetDevice");
+    // fast modes: every matrix rounded onto its per-row, per-component grids
+    std::vector<double> qcols, qx0;
+    if ((flags & PK_FLAG_EXACT) == 0 && n >= pk::kC128NMin) {
+      qcols.resize(ncol * batch);
+      qx0.resize(2 * (size_t)n * batch);
+      for (int b = 0; b < batch; ++b)
+        quantize_walk(cols + (size_t)b * ncol, x0 + 2 * (size_t)b * n, n, 2,
+                      qcols.data() + (size_t)b * ncol, qx0.data() + 2 * (size_t)b * n);
+      cols = qcols.data();
+      x0 = qx0.data();
+    }
     const size_t in_doubles = ncol * batch + 2 * (size_t)n * batch;
     ensure(c.scratch, c.scratch_cap, in_doubles * 8 + 64);
     double* d_cols = (double*)c.scratch;

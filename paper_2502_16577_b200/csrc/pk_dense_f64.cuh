@@ -38,7 +38,6 @@ struct DenseF64Params {
   unsigned long long num_groups;  // groups of 32 consecutive chunks
   unsigned long long g_end;       // inclusive last iterate of the walk
   int k;                          // log2 chunk size, k > LOGU
-  int rb;                         // state rebuild period (log2 steps), 0 = none
 };
 
 template <int N, int PS>
@@ -158,50 +157,6 @@ struct DenseWalk {
     }
   }
 
-  // Periodic state rebuild (fast modes): every 2^rb
-  // steps x is recomputed from scratch instead of carrying the rounding of
-  // all earlier incremental updates. The chunk-constant part -- x0 plus the
-  // columns of gray(base) at bits >= k -- is stashed once per chunk in shared
-  // memory (one slot per thread, stride BLOCK); a rebuild adds the columns of
-  // the iterate's Gray bits below k to it.
-  __device__ __forceinline__ void stash_high(const double* x0, uint64_t base, int k,
-                                             double* sxs) {
-    constexpr int NP = smem_stride<N>();
-#pragma unroll
-    for (int i = 0; i < N; ++i) x[i] = x0[i];
-    // set Gray bits >= k, ascending (ffs walk: one iteration per column)
-    for (uint64_t code = ((base ^ (base >> 1)) >> k) << k; code; code &= code - 1) {
-      const int j = __ffsll((long long)code) - 1;
-      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
-#pragma unroll
-      for (int i = 0; i < N; i += 2) {
-        const double2 v = c2[i / 2];
-        x[i] = __dadd_rn(x[i], v.x);
-        if (i + 1 < N) x[i + 1] = __dadd_rn(x[i + 1], v.y);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) sxs[i * C::BLOCK] = x[i];
-  }
-
-  __device__ __forceinline__ void rebuild(uint64_t g, int k, const double* sxs) {
-    constexpr int NP = smem_stride<N>();
-#pragma unroll
-    for (int i = 0; i < N; ++i) x[i] = sxs[i * C::BLOCK];
-    // set Gray bits < k, ascending (warp-uniform: g is the same for all lanes
-    // up to the chunk base, whose bits < k are zero)
-    for (uint64_t code = (g ^ (g >> 1)) & ((1ull << k) - 1); code; code &= code - 1) {
-      const int j = __ffsll((long long)code) - 1;
-      const double2* c2 = reinterpret_cast<const double2*>(scols + j * NP);
-#pragma unroll
-      for (int i = 0; i < N; i += 2) {
-        const double2 v = c2[i / 2];
-        x[i] = __dadd_rn(x[i], v.x);
-        if (i + 1 < N) x[i + 1] = __dadd_rn(x[i + 1], v.y);
-      }
-    }
-  }
-
   // fold the current state's signed product (term sign = iterate parity)
   __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
     if constexpr (C::QF) {
@@ -285,38 +240,33 @@ struct StaticSteps<N, C, U, U> {
 };
 
 // Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
-// g_end); returns its normalised partial (parallel.py:282-289).
-// rb > 0 (fast modes): the state is rebuilt from the stash sxs every 2^rb
-// steps (rb >= LOGU); rb = 0 walks the chunk incrementally like the reference.
+// g_end) incrementally from its jump-in state, like run_range; returns its
+// normalised partial (parallel.py:282-289). In the fast modes the host has
+// rounded the inputs onto per-row fixed-point grids (quantize_walk in
+// pk_abi.cu), which makes every state of the walk -- and so every DADD of
+// the jump-in and of the updates -- exact: x never drifts.
 template <int N, class C>
 __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0, int k,
-                                           uint64_t g_end, uint64_t c, int rb = 0,
-                                           double* sxs = nullptr) {
+                                           uint64_t g_end, uint64_t c) {
   constexpr int LOGU = C::LOGU;
   constexpr int U = 1 << LOGU;
   DenseWalk<N, C> w(scols);
   const uint64_t base = c << k;
-  if (rb > 0) w.stash_high(x0, base, k, sxs);
-  else w.jump_in(x0, base);
+  w.jump_in(x0, base);
   const uint64_t nbody = 1ull << (k - LOGU);
-  // segments of bodies between rebuilds: the inner loop is the plain walk
-  const uint64_t seg = rb > 0 && rb - LOGU < k - LOGU ? (1ull << (rb - LOGU)) : nbody;
-  for (uint64_t m0 = 0; m0 < nbody; m0 += seg) {
-    if (rb > 0) w.rebuild(base + (m0 << LOGU), k, sxs);
-    for (uint64_t m = m0; m < m0 + seg; ++m) {
-      const uint64_t gb = base + (m << LOGU);
-      const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
-      const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
-      StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
-      // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
-      const uint64_t g = gb + U;
-      if (m + 1 < nbody || g <= g_end) {
-        const int j = changed_col(g);
-        w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
-        w.fold(false, false);
-      }
-      w.end_body();
+  for (uint64_t m = 0; m < nbody; ++m) {
+    const uint64_t gb = base + (m << LOGU);
+    const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
+    const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
+    StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
+    // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
+    const uint64_t g = gb + U;
+    if (m + 1 < nbody || g <= g_end) {
+      const int j = changed_col(g);
+      w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);
+      w.fold(false, false);
     }
+    w.end_body();
   }
   return w.acc.partial();
 }
@@ -337,11 +287,29 @@ __host__ __device__ constexpr size_t dense_cols_doubles() {
   return (size_t)(N - 1) * smem_stride<N>();
 }
 
+// fixed-point image of the precise mode (pk_precise.cuh): (N-1) columns at the
+// smem stride, X0[N], 2^-F[N]
+template <int N>
+__host__ __device__ constexpr size_t fix_words() {
+  return (size_t)(N - 1) * smem_stride<N>() + 2 * N;
+}
+
+// stage the host image (dense [j*N + i] columns, X0, scales) at the smem stride
+template <int N>
+__device__ __forceinline__ void stage_fix(long long* sfix, const long long* fix) {
+  constexpr int NP = smem_stride<N>();
+  for (int t = threadIdx.x; t < (N - 1) * NP; t += blockDim.x) {
+    const int j = t / NP, i = t % NP;
+    sfix[t] = (i < N) ? fix[j * N + i] : 0ll;
+  }
+  for (int t = threadIdx.x; t < 2 * N; t += blockDim.x)
+    sfix[(N - 1) * NP + t] = fix[(N - 1) * N + t];
+}
+
 template <int N, class C>
 __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_f64_chunks(const __grid_constant__ DenseF64Params<N> p) {
   extern __shared__ __align__(16) double scols[];
-  double* sxs = scols + dense_cols_doubles<N>() + threadIdx.x;  // rebuild stash
   stage_columns<N>(scols, p.cols);
   __syncthreads();
   const unsigned int lane = threadIdx.x & 31u;
@@ -349,7 +317,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t grp = warp; grp < p.num_groups; grp += nwarps) {
     const uint64_t c = p.chunk_lo + grp * 32 + lane;
-    dd_t part = walk_chunk<N, C>(scols, p.x0, p.k, p.g_end, c, p.rb, sxs);
+    dd_t part = walk_chunk<N, C>(scols, p.x0, p.k, p.g_end, c);
     if (p.chunk_part) p.chunk_part[grp * 32 + lane] = part;
     part = warp_tree_dd(part);
     if (lane == 0) p.group_part[grp] = part;
@@ -359,7 +327,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
 
 template <int N>
 __host__ __device__ constexpr size_t dense_smem_bytes() {
-  return sizeof(double) * (N - 1) * smem_stride<N>();
+  return sizeof(double) * dense_cols_doubles<N>();
 }
 
 // ---------------------------------------------------------------------------
@@ -376,7 +344,6 @@ struct DenseBatchParams {
   dd_t* out;            // [batch] partial over [1, 2^(N-1)-1]
   int batch;
   int k;
-  int rb;               // state rebuild period (log2 steps), 0 = none
 };
 
 template <int N, class C>
@@ -384,8 +351,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     dense_f64_batch(const __grid_constant__ DenseBatchParams<N> p) {
   extern __shared__ __align__(16) double smem[];
   double* scols = smem;
-  double* sx0 = smem + (N - 1) * smem_stride<N>();
-  double* sxs = sx0 + N + threadIdx.x;  // rebuild stash (stride BLOCK)
+  double* sx0 = smem + dense_cols_doubles<N>();
   const uint64_t total = (1ull << (N - 1)) - 1;
   const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -396,7 +362,7 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
     __syncthreads();
     dd_t* gp = p.group_part + (size_t)b * groups;
     for (int grp = wib; grp < groups; grp += wpb) {
-      dd_t part = walk_chunk<N, C>(scols, sx0, p.k, total, (uint64_t)grp * 32 + lane, p.rb, sxs);
+      dd_t part = walk_chunk<N, C>(scols, sx0, p.k, total, (uint64_t)grp * 32 + lane);
       part = warp_tree_dd(part);
       if (lane == 0) gp[grp] = part;
     }

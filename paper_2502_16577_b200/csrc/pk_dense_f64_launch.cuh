@@ -11,8 +11,7 @@ namespace pk {
 template <int N, class C>
 static int launch_cfg(const DenseLaunch& a, const DenseF64Params<N>& p) {
   auto kern = dense_f64_chunks<N, C>;
-  // columns + the per-thread rebuild stash (fast modes)
-  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * C::BLOCK;
+  constexpr size_t smem = dense_smem_bytes<N>();
   static std::atomic<int> slots[kMaxDevices];  // per device ordinal
   int occ = 1;
   if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
@@ -42,7 +41,6 @@ int launch_dense_f64(const DenseLaunch& a) {
   p.num_groups = a.num_groups;
   p.g_end = a.g_end;
   p.k = a.k;
-  p.rb = a.exact ? 0 : a.rb;
   switch (a.policy) {
     case POL_DD:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
@@ -64,7 +62,7 @@ int launch_dense_f64(const DenseLaunch& a) {
 template <int N, class C>
 static int launch_batch_cfg(const DenseBatchLaunch& a) {
   auto kern = dense_f64_batch<N, C>;
-  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N * (1 + C::BLOCK);
+  constexpr size_t smem = dense_smem_bytes<N>() + sizeof(double) * N;  // + x0
   static std::atomic<int> slots[kMaxDevices];  // per device ordinal
   int occ = 1;
   if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
@@ -75,7 +73,6 @@ static int launch_batch_cfg(const DenseBatchLaunch& a) {
   p.out = a.out;
   p.batch = a.batch;
   p.k = a.k;
-  p.rb = a.exact ? 0 : a.rb;
   uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
   if ((uint64_t)a.batch < grid) grid = a.batch;
   kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);

@@ -26,7 +26,9 @@ inline int prep_kernel(K kern, int block, size_t smem, std::atomic<int>* slots, 
   if (dev < 0 || dev >= kMaxDevices) return (int)cudaErrorInvalidDevice;
   int o = slots[dev].load(std::memory_order_acquire);
   if (o <= 0) {
-    if (smem > 48 * 1024) {
+    // opt in whenever there is dynamic shared memory: the 48 KB default
+    // covers static + dynamic together
+    if (smem > 0) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return (int)e;
     }
@@ -57,10 +59,6 @@ constexpr int dense_block_minb(int N) { return N <= 32 ? 3 : 1; }
 // bodies (profiles/r01_qf_sweep.txt)
 constexpr int qf_logu(int N) { return N <= 36 ? 2 : 3; }
 
-// state rebuild period of the fast modes (log2 steps): x is recomputed from
-// scratch every 2^dense_rebuild_log2 steps instead of drifting over a whole
-// chunk (profiles/r01_accuracy_probe.txt)
-constexpr int kDenseRebuildLog2 = 8;
 
 struct DenseLaunch {
   const double* cols;   // host, (n-1)*n
@@ -68,7 +66,6 @@ struct DenseLaunch {
   int policy;
   bool exact;
   int k;                // log2 chunk size, k > dense_logu(n)
-  int rb;               // rebuild period (log2 steps) in fast mode, 0 = none
   uint64_t chunk_lo;
   uint64_t num_groups;  // groups of 32 chunks
   uint64_t g_end;
@@ -84,6 +81,24 @@ struct DenseLaunch {
 template <int N>
 int launch_dense_f64(const DenseLaunch& a);
 
+// precise mode (pk_precise.cuh): exact fixed-point row sums, double-double
+// products and sums; any order in [kDenseNMin, kDenseNMax]
+struct PreciseLaunch {
+  const long long* fix;  // device fixed-point image (fixed_image in pk_abi.cu)
+  int k;
+  uint64_t chunk_lo;
+  uint64_t num_groups;
+  uint64_t g_end;
+  dd_t* group_part;
+  dd_t* chunk_part;
+  dd_t* out;
+  unsigned int* counter;
+  cudaStream_t stream;
+  int sms;
+};
+
+int launch_dense_f64_precise(int n, const PreciseLaunch& a);
+
 // batched whole walks of `batch` matrices of order N (device inputs)
 struct DenseBatchLaunch {
   const double* d_cols;  // [batch][(N-1)*N]
@@ -92,7 +107,6 @@ struct DenseBatchLaunch {
   bool exact;
   int batch;
   int k;
-  int rb;                // rebuild period (log2 steps) in fast mode, 0 = none
   dd_t* group_part;      // [batch][2^(N-1-k)/32]
   dd_t* out;             // [batch]
   cudaStream_t stream;

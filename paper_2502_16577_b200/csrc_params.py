@@ -23,3 +23,7 @@ def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:
     length has `bit_len` bits (a whole walk: n - 1)."""
     k = max(bit_len - chunks_log2, min(12, bit_len - 17))
     return max(k, logu + 1)
+
+
+# largest order with complex register kernels (pk_launch.h kC128NMax)
+C128_N_MAX = 40

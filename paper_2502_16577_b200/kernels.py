@@ -157,14 +157,16 @@ class DenseF64Problem:
 
     def walk(self, start: int, end: int, policy: AccumulatorPolicy, *, exact: bool = False,
              devices: Optional[Sequence[int]] = None, log2_chunk: int = 0,
-             stats: Optional[nat.RunStats] = None) -> DoubleDouble:
+             stats: Optional[nat.RunStats] = None, precise: bool = False) -> DoubleDouble:
+        """precise=True: exact fixed-point row sums, double-double products and
+        sums (PK_FLAG_PRECISE; the policy is then irrelevant)."""
         lib = nat.load()
         out = np.zeros(2)
         dptr, nd, _keep = nat.devices_arg(devices)
         st = stats if stats is not None else nat.RunStats()
+        flags = (nat.PK_FLAG_EXACT if exact else 0) | (nat.PK_FLAG_PRECISE if precise else 0)
         rc = lib.pk_dense_f64(nat.dptr(self.cols), nat.dptr(self.x0), self.n, start, end,
-                              policy.code, nat.PK_FLAG_EXACT if exact else 0, log2_chunk,
-                              dptr, nd, nat.dptr(out), st)
+                              policy.code, flags, log2_chunk, dptr, nd, nat.dptr(out), st)
         nat.check(rc, "pk_dense_f64")
         return DoubleDouble(float(out[0]), float(out[1]))
 
@@ -185,14 +187,15 @@ class DenseF64Problem:
     flags = 0  # PK_FLAG_SPARSE for the SpaRyser subclass
 
     def chunks(self, log2_chunk: int, chunk_lo: int, nchunks: int, policy: AccumulatorPolicy,
-               exact: bool = True, device: int = 0):
+               exact: bool = True, device: int = 0, precise: bool = False):
         """Per-chunk partials of the register kernel (parity diagnostics)."""
         lib = nat.load()
         out = np.zeros(2 * nchunks)
         tot = np.zeros(2)
+        flags = self.flags | (nat.PK_FLAG_EXACT if exact else 0) | \
+            (nat.PK_FLAG_PRECISE if precise else 0)
         rc = lib.pk_dense_f64_chunks(nat.dptr(self.cols), nat.dptr(self.x0), self.n, log2_chunk,
-                                     chunk_lo, nchunks, policy.code,
-                                     self.flags | (nat.PK_FLAG_EXACT if exact else 0), device,
+                                     chunk_lo, nchunks, policy.code, flags, device,
                                      nat.dptr(out), nat.dptr(tot))
         nat.check(rc, "pk_dense_f64_chunks")
         return out.reshape(-1, 2), DoubleDouble(float(tot[0]), float(tot[1]))
@@ -243,21 +246,27 @@ class SparseF64Problem(DenseF64Problem):
 
 
 def _real_walk_total(a: DenseMatrix, policy: AccumulatorPolicy, devices=None,
-                     stats: Optional[nat.RunStats] = None) -> float:
+                     stats: Optional[nat.RunStats] = None, precise: bool = False) -> float:
     n = a.n
     prob = DenseF64Problem(a)
-    p0 = policy_product(prob.x0, policy)
+    # precise mode: the g = 0 product in double-double as well
+    p0 = policy_product(prob.x0, AccumulatorPolicy.QQ if precise else policy)
     acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
     if n > 1:
-        acc = dd_add(acc, prob.walk(1, total_iterates(n), policy, devices=devices, stats=stats))
+        acc = dd_add(acc, prob.walk(1, total_iterates(n), policy, devices=devices, stats=stats,
+                                    precise=precise))
     return acc.hi * _sign_factor(n)
 
 
 def perm_nw(a: DenseMatrix, policy: "AccumulatorPolicy | str" = AccumulatorPolicy.DD,
-            *, devices: Optional[Sequence[int]] = None) -> Scalar:
+            *, devices: Optional[Sequence[int]] = None, precise: bool = False) -> Scalar:
     """Permanent by the Gray walk over the 2^(n-1) half-space subsets,
-    computed on the GPU (kernels.py:297-324)."""
+    computed on the GPU (kernels.py:297-324). precise=True (dense real,
+    n >= 11): exact fixed-point row sums with double-double products and sums
+    -- reference-grade, about 12x slower."""
     policy = as_policy(policy)
+    if precise and a.kind != KIND_REAL:
+        raise PolicyError("precise mode serves dense real matrices")
     if a.kind == KIND_INT:
         from .integer import int_walk_total
         return int_walk_total(a, devices=devices)
@@ -266,7 +275,7 @@ def perm_nw(a: DenseMatrix, policy: "AccumulatorPolicy | str" = AccumulatorPolic
             raise PolicyError("complex matrices support the plain-double policy only")
         from .complex_walk import complex_walk_total
         return complex_walk_total(a, devices=devices)
-    return _real_walk_total(a, policy, devices)
+    return _real_walk_total(a, policy, devices, precise=precise)
 
 
 def perm_spa(s: SparsePair, policy: "AccumulatorPolicy | str" = AccumulatorPolicy.DD,

@@ -177,11 +177,11 @@ def test_errors_are_the_reference_classes():
         prob.chunks(3, 0, 32, AccumulatorPolicy.DD)  # k below the body length
 
 
-def test_state_rebuild_removes_chunk_length_drift():
-    # fast mode rebuilds x every 2^8 steps: the result
-    # no longer depends on the chunk length at the 1e-10 level, where the
-    # incremental walk of 2^k-step chunks drifted by ~1e-9 (n = 36, k = 16;
-    # profiles/r01_accuracy_probe.txt)
+def test_fast_states_are_exact_so_chunk_length_does_not_matter():
+    # fast mode walks the input rounded onto per-row grids on which every
+    # state is a double (pk_abi.cu quantize_walk): x never
+    # drifts, so the chunk length only reorders the product sums. The
+    # reference's incremental walk of 2^k-step chunks drifted by ~1e-9 here.
     n = 34
     g = np.random.default_rng(20261017).uniform(0.0, 1.0, size=(n, n))
     m = pk.DenseMatrix.from_array(g)
@@ -193,4 +193,23 @@ def test_state_rebuild_removes_chunk_length_drift():
         part = prob.walk(1, T, AccumulatorPolicy.KAHAN, log2_chunk=k)
         vals.append(dd_add(DoubleDouble(p0, 0.0), part).hi)
     for v in vals[1:]:
-        assert abs(v - vals[0]) <= 1e-10 * abs(vals[0]), vals
+        assert abs(v - vals[0]) <= 1e-12 * abs(vals[0]), vals
+
+
+@pytest.mark.parametrize("n", [24, 30, 34])
+def test_fast_within_1e11_of_precise_mode(n):
+    # precise mode: exact fixed-point row sums, double-double products and
+    # sums (pk_precise.cuh) -- the reference-grade value
+    g = np.random.default_rng(77 + n).uniform(0.0, 1.0, size=(n, n))
+    m = pk.DenseMatrix.from_array(g)
+    want = pk.perm_nw(m, precise=True)
+    for p in POLS:
+        got = pk.perm_nw(m, p)
+        assert rel(got, want) <= 1e-11, (n, p, got, want, rel(got, want))
+
+
+@pytest.mark.parametrize("n", [16, 24, 30])
+def test_precise_mode_uniform_closed_form(n):
+    exact = math.factorial(n) * Fraction(0.91) ** n
+    got = pk.perm_nw(pk.uniform(n, 0.91), precise=True)
+    assert float(abs(Fraction(got) - exact) / exact) <= 1e-14
