@@ -203,7 +203,7 @@ def _reference_importable():
     return False
 
 
-def cpu_updates_per_s(n: int, policy: str, sample_log2: int, rows):
+def cpu_updates_per_s(n: int, policy: str, sample_log2: int, rows, force_port: bool = False):
     """Time the reference CPU implementation on a bounded, contiguous sample
     of the n-walk (2^sample_log2 iterates from g=1) split over all host
     cores. Uses permkit itself (numba JIT, execute_plan's thread-pool
@@ -215,7 +215,7 @@ def cpu_updates_per_s(n: int, policy: str, sample_log2: int, rows):
     size = max(1, count // nchunks)
     spans = [(1 + i * size, (i + 1) * size) for i in range(nchunks)]
     updates = size * nchunks
-    if _reference_importable():
+    if not force_port and _reference_importable():
         from concurrent.futures import ThreadPoolExecutor
         import permkit
         from permkit.parallel import run_range
@@ -265,6 +265,15 @@ def run_reference(args, dist: Dist):
             samples.append(r)
     ups = statistics.median(s["value"] for s in samples)
     total = (1 << (args.n - 1)) - 1
+    impl = {"reference": "permkit 0.1.0, numba JIT loops (baseline/_ref, the reference's own "
+                         "code) on a thread pool",
+            "port": "oracle/permref.c (C restatement of permkit's loop; permkit not installed)"}
+    extra = {}
+    if samples[-1]["kind"] == "reference":
+        # how the C port compares with the real reference on this host (the
+        # round-1 arm used the port when permkit was absent)
+        port = cpu_updates_per_s(args.n, args.policy, log2 - 2, rows, force_port=True)
+        extra = {"port_updates_per_s": port["value"], "port_over_reference": port["value"] / ups}
     line = {
         "impl": "reference", "metric": METRIC, "value": ups, "unit": "updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -274,8 +283,9 @@ def run_reference(args, dist: Dist):
                                f"policy {args.policy}; per step a bounded sample of the walk "
                                f"on the host cores (extrapolated ms_per_step)",
                    "n": args.n, "policy": args.policy},
-        "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {"value": ups,
-                                                                                    "unit": "updates/s"},
+        "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {
+            "value": ups, "unit": "updates/s", "implementation": impl[samples[-1]["kind"]],
+            **extra},
         "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -393,9 +403,10 @@ class Workload:
         y = (total << self.even_rows) + IntProblem(self.m).p0_y()
         return str(finalize_int(y, n))
 
-    def public_call(self):
+    def public_call(self, workers=1):
         import paper_2502_16577_b200 as pk
-        return pk.permanent(self.m if self.kind != "dense" else self.rows, self.policy)
+        return pk.permanent(self.m if self.kind != "dense" else self.rows, self.policy,
+                            workers=workers)
 
     def input_bytes(self):
         n = self.n
@@ -411,7 +422,7 @@ class Workload:
 
 # ncu --set full summaries of each workload's dominant kernel (profiles/):
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch
-NCU_SUMMARY = {"dense": "r01_ncu_k1_full_summary.csv", "sparse": "r01_ncu_spa_f64_full_summary.csv",
+NCU_SUMMARY = {"dense": "r02_ncu_k1_full_summary.csv", "sparse": "r02_ncu_spa_f64_full_summary.csv",
                "haar": "r01_ncu_k3_full_summary.csv", "binary": "r01_ncu_k6_full_summary.csv"}
 
 
@@ -469,9 +480,13 @@ def run_b200(args, dist: Dist):
     flusher = L2Flusher(dist.device)
 
     def step_e2e():
+        # the public API from a host matrix: at N > 1 rank 0 calls
+        # permanent(..., workers=N) over all N GPUs in-process (one host thread
+        # per device) while the other ranks wait at the barrier
         t0 = time.perf_counter()
-        if N == 1 and not args.range_log2:
-            wl.public_call()
+        if not args.range_log2:
+            if rank == 0:
+                wl.public_call(N)
         else:
             wl.walk(lo, hi, dev)
         return (time.perf_counter() - t0) * 1e3
@@ -588,8 +603,9 @@ def run_b200(args, dist: Dist):
         "e2e": {"value": e2e_ups, "unit": "updates/s",
                 "h2d_bytes_per_step": wl.input_bytes() * N, "d2h_bytes_per_step": 48 * N,
                 "ms_per_step": statistics.mean(step_e),
-                "path": "paper_2502_16577_b200.permanent(host matrix) at N=1; per-rank range "
-                        "walk through the C ABI at N>1"},
+                "path": "paper_2502_16577_b200.permanent(host matrix, workers=N): H2D of the "
+                        "inputs, the walk over N GPUs (one host thread each), D2H of the "
+                        "partials, host combination"},
         "gpu_launches": int(sum(g[0] for g in g_launch)),
         "clocks": clocks.summary(),
     }

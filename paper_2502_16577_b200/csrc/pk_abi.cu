@@ -481,7 +481,6 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
                   uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
       pk::SpaF64Launch a{};
-      a.rb = 0;  // exact states: nothing to rebuild
       a.d_cols = d_in;
       a.d_x0 = d_in + nc;
       a.d_vals = d_in + voff;

@@ -52,7 +52,6 @@ struct SpaF64Spec {
 std::vector<int> spa_f64_offsets(const SpaF64Spec& sp, int* total);
 
 struct SpaF64Launch {
-  int rb;                // state rebuild period (log2 steps) in fast mode
   const double* d_cols;  // device dense (n-1)*n columns (jump-in)
   const double* d_x0;    // device seed x0[n]
   const double* d_vals;  // device packed nonzeros (spa_f64_offsets layout)
