@@ -338,10 +338,11 @@ class Workload:
         chunks for real / integer walks, 2^19 for complex; pk_abi.cu
         plan_dense). Every rank uses it, so an N-rank split walks exactly the
         single-GPU chunks and reproduces its bits (power-of-two N)."""
-        from paper_2502_16577_b200.csrc_params import auto_log2_chunk, c128_logu, dense_logu
+        from paper_2502_16577_b200.csrc_params import (auto_log2_chunk, c128_register_logu,
+                                                       dense_logu)
         n = self.n
         if self.kind == "haar":
-            return auto_log2_chunk(n - 1, c128_logu(n), 19)
+            return auto_log2_chunk(n - 1, c128_register_logu(n), 19)
         logu = 2 if self.kind == "binary" else dense_logu(n)
         return auto_log2_chunk(n - 1, logu, 22)
 
@@ -596,6 +597,13 @@ def run_b200(args, dist: Dist):
                   "int128 products, 192-bit sums"}[wl.kind],
         "data": "synthetic",
         "config": {"workload": wl.desc, "n": n, "policy": wl.policy,
+                   "accumulation": ("fast mode: inputs rounded onto per-row grids so every "
+                                    "row-sum state is exact; 16-term body sums in double "
+                                    "folded into the policy's accumulator once per body"
+                                    if wl.kind in ("dense", "sparse") else
+                                    "fast mode: exact states; plain complex body sums, "
+                                    "compensated per component" if wl.kind == "haar" else
+                                    "exact 192-bit integer sums"),
                    "split": f"{N} contiguous power-of-two iterate ranges, one per GPU",
                    "log2_chunk": k_used, "l2": "flushed (256 MiB write) between steps",
                    "permanent": result},

@@ -357,6 +357,49 @@ int dispatch_int_batch(int n, const pk::IntBatchLaunch& a) {
   }
 }
 
+int dispatch_c128_pair(int n, const pk::C128Launch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_c128_pair<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40) PK_CASE(41) PK_CASE(42) PK_CASE(43) PK_CASE(44) PK_CASE(45)
+    PK_CASE(46) PK_CASE(47) PK_CASE(48) PK_CASE(49) PK_CASE(50) PK_CASE(51) PK_CASE(52)
+    PK_CASE(53) PK_CASE(54) PK_CASE(55) PK_CASE(56) PK_CASE(57) PK_CASE(58) PK_CASE(59)
+    PK_CASE(60) PK_CASE(61) PK_CASE(62) PK_CASE(63)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+// Complex register kernel for order n: K3 (one thread per chunk) up to
+// kC128NMax, the lane-pair kernel K3p above (PK_C128_PAIR=1 selects K3p for
+// every order, for A/B runs).
+// K3's fast product schedule: 2 one chain (default), 0 two chains (TC), 1
+// one chain with the fused last multiply (FA). Measured at n = 24..36
+// (profiles/r02_c128_variants.txt): TC -1..-8 %, FA within 1 % of the
+// default. PK_C128_VARIANT overrides it for A/B runs.
+int c128_variant() {
+  static const int v = [] {
+    const char* e = getenv("PK_C128_VARIANT");
+    const int r = e ? atoi(e) : 2;
+    return (r >= 0 && r <= 2) ? r : 2;
+  }();
+  return v;
+}
+
+bool c128_use_pair(int n) {
+  static const bool all = [] {
+    const char* e = getenv("PK_C128_PAIR");
+    return e && atoi(e) == 1;
+  }();
+  return n >= pk::kC128NMin && n <= pk::kDenseNMax && (all || n > pk::kC128NMax);
+}
+
 int dispatch_c128_batch(int n, const pk::C128BatchLaunch& a) {
   switch (n) {
 #define PK_CASE(N) \
@@ -584,7 +627,9 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   Kind kd;
   kd.n = n;
   kd.streams = 2;
-  kd.logu = (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
+  const bool pair = c128_use_pair(n);
+  kd.logu = pair ? pk::c128_pair_logu(n)
+                 : (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
   kd.chunks_log2 = 19;
   const size_t nc = 2 * ncols_of(n);
   // fast modes walk the input rounded onto per-row, per-component grids
@@ -599,10 +644,11 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 16);
   const double* h_x0 = x0;
-  if (sparse && kd.logu > 0) {
+  if (sparse && kd.logu > 0 && !pair) {
     // SpaRyser: generated kernel over the nonzero pattern; packed nonzeros
     // (interleaved re, im) appended to the inputs
     auto sp = std::make_shared<pk::SpaC128Spec>(spa_c128_spec(cols, n, exact));
+    sp->variant = c128_variant();
     const size_t voff = kd.input.size();
     for (int j = 0; j < n - 1; ++j)
       for (int r : sp->rows[j]) {
@@ -635,6 +681,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
                 uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
     (void)qbuf;  // keeps the rounded inputs alive with the lambda
     pk::C128Launch a{};
+    a.variant = c128_variant();
     a.d_cols = d_in;
     a.x0 = h_x0;
     a.exact = exact;
@@ -648,7 +695,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
     a.counter = c.counter;
     a.stream = c.stream;
     a.sms = c.sms;
-    return dispatch_c128(n, a);
+    return pair ? dispatch_c128_pair(n, a) : dispatch_c128(n, a);
   };
   }
   kd.walk = [=](DevCtx& c, const double* d_in, const unsigned long long* d_s,

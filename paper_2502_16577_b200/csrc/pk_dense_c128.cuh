@@ -40,11 +40,17 @@ struct DenseC128Params {
 // FA (fast mode): the last complex multiply of each product and the body sum
 // fold into four DFMAs, b += (+-p) * x[N-1] per component (two FP64
 // instructions fewer per update)
-template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false, int BLOCK_ = kC128Block>
+// TC (fast mode): the product runs as two interleaved chains over the even
+// and the odd rows, and four DFMAs multiply them into the body sum -- the
+// same FP64 instruction count as FA, twice the independent work per term
+// (the single chain is latency bound at 2 warps per scheduler)
+template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false, int BLOCK_ = kC128Block,
+          bool TC_ = false>
 struct C128Cfg {
   static constexpr int LOGU = LOGU_, MINB = MINB_, BLOCK = BLOCK_;
   static constexpr bool EXACT = EXACT_;
-  static constexpr bool FA = FA_ && !EXACT_;
+  static constexpr bool TC = TC_ && !EXACT_;
+  static constexpr bool FA = FA_ && !EXACT_ && !TC;
 };
 
 // complex partial sum: plain (reference) or compensated per component
@@ -145,6 +151,26 @@ struct C128Walk {
   }
 
   __device__ __forceinline__ void fold(bool odd, bool first_in_body) {
+    if constexpr (C::TC) {
+      double er = xr[0], ei = xi[0], orr = xr[1], oi = xi[1];
+#pragma unroll
+      for (int i = 2; i < N; ++i) {
+        double& pr = (i & 1) ? orr : er;
+        double& pi = (i & 1) ? oi : ei;
+        const double r = __fma_rn(pr, xr[i], -__dmul_rn(pi, xi[i]));
+        const double m = __fma_rn(pr, xi[i], __dmul_rn(pi, xr[i]));
+        pr = r;
+        pi = m;
+      }
+      if (odd) {
+        er = -er;
+        ei = -ei;
+      }
+      const double r0 = first_in_body ? 0.0 : br, i0 = first_in_body ? 0.0 : bi;
+      br = __fma_rn(er, orr, __fma_rn(-ei, oi, r0));
+      bi = __fma_rn(er, oi, __fma_rn(ei, orr, i0));
+      return;
+    }
     if constexpr (C::FA) {
       double pr = xr[0], pi = xi[0];
 #pragma unroll

@@ -144,10 +144,20 @@ struct C128Launch {
   unsigned int* counter;
   cudaStream_t stream;
   int sms;
+  int variant;           // fast-mode product schedule of K3 (pk_dense_c128_launch.cuh)
 };
 
 template <int N>
 int launch_dense_c128(const C128Launch& a);
+
+// lane-pair complex kernel (pk_c128_pair.cuh): every order up to kDenseNMax;
+// 4*ceil(N/2) registers of state per lane
+constexpr int c128_pair_logu(int N) { return N <= 48 ? 2 : 1; }
+constexpr int c128_pair_block(int N) { return 256; }
+constexpr int c128_pair_minb(int N) { return N <= 32 ? 2 : 1; }
+
+template <int N>
+int launch_c128_pair(const C128Launch& a);
 
 // batched whole complex walks of `batch` matrices of order N (device inputs)
 struct C128BatchLaunch {

@@ -83,6 +83,7 @@ struct SpaC128Spec {
   int n = 0;
   std::vector<std::vector<int>> rows;  // nonzero rows of column j < n-1
   bool exact = false;
+  int variant = 0;  // fast-mode product schedule, as K3's C128Launch::variant
 };
 
 struct SpaC128Launch {

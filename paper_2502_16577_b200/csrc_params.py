@@ -25,5 +25,16 @@ def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:
     return max(k, logu + 1)
 
 
-# largest order with complex register kernels (pk_launch.h kC128NMax)
+# largest order of the one-thread-per-chunk complex kernel K3 (pk_launch.h
+# kC128NMax); orders above it run the lane-pair kernel K3p up to 63
 C128_N_MAX = 40
+C128_PAIR_N_MAX = 63
+
+
+def c128_pair_logu(n: int) -> int:
+    return 2 if n <= 48 else 1
+
+
+def c128_register_logu(n: int) -> int:
+    """Body length exponent of the complex register kernel the library runs at order n."""
+    return c128_logu(n) if n <= C128_N_MAX else c128_pair_logu(n)

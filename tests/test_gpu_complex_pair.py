@@ -1,0 +1,72 @@
+"""The lane-pair complex kernel K3p (csrc/pk_c128_pair.cuh): register walks of
+complex matrices of order 41..63, where one thread's 4n registers of state no
+longer fit. Exact mode keeps the reference's sequential
+product across the two lanes and must reproduce run_range over every chunk
+bit for bit (the C oracle restates chunk_dense_c128, _loops.py:186-209);
+fast mode (exact grid-rounded states, fma products, compensated body sums)
+must agree with it."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2502_16577_b200 as pk
+from paper_2502_16577_b200.complex_walk import DenseC128Problem
+from paper_2502_16577_b200.precision import dd_pairwise
+
+pytestmark = pytest.mark.gpu
+
+
+def _haar(n, seed):
+    m = pk.haar_unitary_block(n, seed, m=2 * n)  # a smaller unitary: larger entries
+    return m, np.array(m.data, dtype=np.complex128).reshape(n, n)
+
+
+@pytest.mark.parametrize("n", [41, 44, 48, 55, 63])
+def test_pair_exact_chunks_bitwise_vs_oracle(n):
+    m, a = _haar(n, 900 + n)
+    prob = DenseC128Problem(m)
+    k = 7
+    total_chunks = 1 << (n - 1 - k)
+    for lo in (0, 1 << 20, total_chunks - 32):  # walk start, middle, last (clipped) chunks
+        parts, (tr, ti) = prob.chunks(k, lo, 32, exact=True)
+        T = (1 << (n - 1)) - 1
+        for i in range(0, 32, 5):
+            c = lo + i
+            s, e = 1 + c * (1 << k), min((c + 1) << k, T)
+            want = oracle.dense_c128_range(a, s, e)
+            assert (parts[i][0].hex(), parts[i][1].hex()) == (want.real.hex(), want.imag.hex()), (n, c)
+        # the launch total is the fixed tree over the chunk partials
+        re = dd_pairwise([(float(p[0]), 0.0) for p in parts])
+        im = dd_pairwise([(float(p[1]), 0.0) for p in parts])
+        assert (re.hi, re.lo, im.hi, im.lo) == (tr.hi, tr.lo, ti.hi, ti.lo)
+
+
+@pytest.mark.parametrize("n", [41, 52])
+def test_pair_fast_chunks_close_to_exact(n):
+    m, _ = _haar(n, 700 + n)
+    prob = DenseC128Problem(m)
+    k = 9
+    lo = 3 << 12
+    fe, _ = prob.chunks(k, lo, 64, exact=True)
+    ff, _ = prob.chunks(k, lo, 64, exact=False)
+    for e, f in zip(fe, ff):
+        ze, zf = complex(e[0], e[1]), complex(f[0], f[1])
+        assert abs(zf - ze) <= 1e-10 * max(abs(ze), 1e-300), (n, ze, zf)
+
+
+def test_pair_whole_walk_n41_fast_vs_exact():
+    # the whole 2^40-iterate walk both ways: fast (exact states) and exact
+    # mode, the reference's incrementally updated states, over 2^10-step
+    # chunks so that its row-sum drift stays small (over the default 2^21-step
+    # chunks the two differ by 3.8e-9: the reference's drift)
+    m, _ = _haar(41, 5)
+    fast = pk.perm_nw(m)
+    prob = DenseC128Problem(m)
+    wr, wi = prob.walk(1, (1 << 40) - 1, exact=True, log2_chunk=10)
+    p0 = prob.p0()
+    from paper_2502_16577_b200.precision import DoubleDouble, dd_add
+    re = dd_add(DoubleDouble(p0.real, 0.0), wr)
+    im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+    exact = complex(re.hi, im.hi) * pk.kernels._sign_factor(41)
+    assert abs(fast - exact) <= 1e-10 * abs(exact), (fast, exact, abs(fast - exact) / abs(exact))

@@ -190,7 +190,7 @@ def _precise(job, m):
 def test_fast_walk_within_tolerance_and_closer_than_the_reference(job):
     # The reference's permanent_chunked walks 2^19 (n = 36) or 2^23 (n = 40)
     # steps per chunk with incrementally updated row sums; its value drifts
-    # from the exact-state value by ~1e-9 (n = 36). The fast walk (exact
+    # from the exact-state value by 1.2e-9 (n = 36) and 5.9e-7 (n = 40). The fast walk (exact
     # states, pk_abi.cu quantize_walk) must agree with the precise value to
     # the north-star tolerance and be at least as close to it as the reference.
     d = load(job)
@@ -198,7 +198,7 @@ def test_fast_walk_within_tolerance_and_closer_than_the_reference(job):
     ref = float.fromhex(d["value"])
     truth = _precise(job, m)
     fast = pk.perm_nw(m, d["policy"])
-    assert abs(ref - truth) <= 1e-7 * abs(truth), (ref, truth)  # same permanent, drift aside
+    assert abs(ref - truth) <= 1e-6 * abs(truth), (ref, truth)  # same permanent, drift aside
     assert abs(fast - truth) <= REL_TOL * abs(truth), (fast, truth, (fast - truth) / truth)
     assert abs(fast - truth) <= abs(ref - truth), (fast, ref, truth)
 
@@ -234,3 +234,15 @@ def test_config4_haar32_fast_vs_reference():
     want = _dec(d["value"], "complex128")
     got = pk.perm_nw(m)
     assert abs(got - want) <= 1e-9 * abs(want), (got, want, abs(got - want) / abs(want))
+
+
+def test_config3_binary40_two_independent_kernels_agree():
+    # the whole 2^39-iterate exact walk of config 3 by the per-matrix generated
+    # SpaRyser kernel (fp32 groups, K6) and by the template dense integer
+    # kernel (int32 groups, K5): two independent exact arithmetics, same
+    # integer; both equal the round-1 bench value
+    from paper_2502_16577_b200.integer import int_walk_total
+    m = pk.dense_to_sparse(pk.random_binary(40, 20261017, 0.3))
+    a = int_walk_total(m, sparse=True)
+    b = int_walk_total(m, sparse=False)
+    assert a == b == 48153712130998394697054824

@@ -75,7 +75,7 @@ def test_walker_register_boundary_real(n):
 
 @pytest.mark.parametrize("n", [39, 40, 41])
 def test_complex_register_boundary(n):
-    # complex register kernels stop at n = 40; n = 41 takes the walkers.
+    # K3 stops at n = 40; n = 41 takes the lane-pair kernel K3p.
     # A unaligned range walked both ways must equal the oracle's partial.
     h = pk.haar_unitary_block(n, 5)
     a = np.array(h.data, dtype=np.complex128).reshape(n, n)
