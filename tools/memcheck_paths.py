@@ -26,4 +26,18 @@ print(pk.permanent_batch([pk.random_real(14, k) for k in range(4)] + [pk.haar_un
 big = pk.random_binary(38, 9, 0.3)
 print(IntProblem(big).walk(1, 1 << 24)[0])
 print(pk.decomp_run(pk.random_sparse_real(16, 0.35, 3, 0.0, 1.0), "kahan")[0])
+# round 2: the large-order block shapes, the precise mode, the lane-pair
+# complex kernel and the grid-rounded fast inputs
+from paper_2502_16577_b200.complex_walk import DenseC128Problem  # noqa: E402
+from paper_2502_16577_b200.kernels import DenseF64Problem, SparseF64Problem  # noqa: E402
+K = pk.AccumulatorPolicy.KAHAN
+for n in (34, 40, 52):
+    prob = DenseF64Problem(pk.random_real(n, 4, 0.0, 1.0))
+    print(n, prob.walk(1, 1 << 22, K), prob.walk(1 << 30, (1 << 30) + (1 << 21) + 77, pk.AccumulatorPolicy.QQ))
+print(DenseF64Problem(pk.random_real(36, 4, 0.0, 1.0)).walk(1, 1 << 20, K, precise=True))
+print(SparseF64Problem(pk.random_sparse_real(36, 0.3, 5, 0.0, 1.0)).walk(1, 1 << 22, K))
+for n in (32, 41, 63):
+    hp = DenseC128Problem(pk.haar_unitary_block(n, 3, m=2 * n))
+    print(n, hp.walk(1, 1 << 21), hp.chunks(7, 32, 32, exact=True)[1])
+print(IntProblem(pk.dense_to_sparse(pk.random_binary(40, 5, 0.3))).walk(1, 1 << 22)[0])
 print("memcheck paths done")
