@@ -257,6 +257,17 @@ typedef struct pk_decomp_result {
   int64_t leaf_values;  /* total scalars of the concatenated leaf matrices */
 } pk_decomp_result;
 
+/* The fast modes' input rounding (host only, no device needed): every
+ * value of row i (component c of interleaved complex data when comps = 2) is
+ * rounded to the grid 2^-F, F = 52 - e, B = |x0_i| + sum_j |a_ij| < 2^e, on
+ * which every subset sum x0_i + sum_{j in S} a_ij -- every state of the
+ * walk -- is a double. cols are the n-1 walked columns (dense_float_state /
+ * dense_complex_state layout), x0 the seed; outputs may alias the inputs.
+ * Replaces nothing in the reference: its walk rounds x at every step
+ * (_loops.py:47-48); DESIGN.md §3 "Exact states". */
+int pk_quantize_walk(const double* cols, const double* x0, int n, int comps, double* qcols,
+                     double* qx0);
+
 /* acc = dd_add(acc, (vals[k], 0)) for k in order from (0, 0) (the robust
  * double-double add of precision.py:84-96): permkit's leaf combination */
 int pk_dd_accumulate(const double* vals, int64_t count, double out[2]);

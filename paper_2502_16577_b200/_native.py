@@ -116,6 +116,7 @@ SIGNATURES = {
     "pk_spa_c128_source": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_uint32, ctypes.c_char_p,
                                           ctypes.c_uint64, _U64]),
     "pk_dd_accumulate": (ctypes.c_int, [_D, ctypes.c_int64, _D]),
+    "pk_quantize_walk": (ctypes.c_int, [_D, _D, ctypes.c_int, ctypes.c_int, _D, _D]),
     "pk_decomp_tree": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                       ctypes.POINTER(ctypes.c_void_p),

@@ -1600,6 +1600,18 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
 
 // acc = dd_add(acc, (v_k, 0)) over k in order, from acc = (0, 0): the
 // reference's leaf combination (preprocess.py:398-417) for one component
+int pk_quantize_walk(const double* cols, const double* x0, int n, int comps, double* qcols,
+                     double* qx0) {
+  return guarded([&] {
+    check_n(n);
+    if (comps != 1 && comps != 2) fail(PK_ERR_ARG, "comps must be 1 (real) or 2 (complex)");
+    if (!x0 || !qx0 || (n > 1 && (!cols || !qcols))) fail(PK_ERR_ARG, "null pointer argument");
+    const size_t nc = (size_t)comps * (n > 1 ? n - 1 : 0) * n;
+    std::vector<double> c(cols, cols + nc), x(x0, x0 + (size_t)comps * n);  // outputs may alias
+    quantize_walk(c.data(), x.data(), n, comps, qcols, qx0);
+  });
+}
+
 int pk_dd_accumulate(const double* vals, int64_t count, double out[2]) {
   return guarded([&] {
     if ((!vals && count > 0) || !out || count < 0) fail(PK_ERR_ARG, "bad arguments");
