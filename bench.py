@@ -404,6 +404,11 @@ class Workload:
         y = (total << self.even_rows) + IntProblem(self.m).p0_y()
         return str(finalize_int(y, n))
 
+    def public_range(self, lo, hi, devices):
+        import paper_2502_16577_b200 as pk
+        return pk.run_range(self.m if self.kind != "dense" else pk.DenseMatrix.from_rows(self.rows),
+                            lo, hi, self.policy, devices=devices)
+
     def public_call(self, workers=1):
         import paper_2502_16577_b200 as pk
         return pk.permanent(self.m if self.kind != "dense" else self.rows, self.policy,
@@ -480,16 +485,27 @@ def run_b200(args, dist: Dist):
     dev = [dist.device]
     flusher = L2Flusher(dist.device)
 
+    # the public API from a host matrix: at N > 1 rank 0 calls
+    # permanent(..., workers=N) over all N GPUs in-process (one host thread per
+    # device) while the other ranks wait at the barrier; if a rank cannot see
+    # N devices, every rank calls the public run_range on its own range
+    import torch
+    in_process = N == 1 or torch.cuda.device_count() >= N
+    e2e_path = ("paper_2502_16577_b200.permanent(host matrix, workers=N): H2D of the inputs, "
+                "the walk over N GPUs (one host thread each), D2H of the partials, host "
+                "combination" if in_process else
+                "paper_2502_16577_b200.run_range(host matrix, rank range) on each rank's GPU "
+                "(H2D inputs, walk, D2H partial)")
+
     def step_e2e():
-        # the public API from a host matrix: at N > 1 rank 0 calls
-        # permanent(..., workers=N) over all N GPUs in-process (one host thread
-        # per device) while the other ranks wait at the barrier
         t0 = time.perf_counter()
-        if not args.range_log2:
+        if args.range_log2:
+            wl.walk(lo, hi, dev)
+        elif in_process:
             if rank == 0:
                 wl.public_call(N)
         else:
-            wl.walk(lo, hi, dev)
+            wl.public_range(lo, hi, dev)
         return (time.perf_counter() - t0) * 1e3
 
     for _ in range(args.warmup):
@@ -611,9 +627,7 @@ def run_b200(args, dist: Dist):
         "e2e": {"value": e2e_ups, "unit": "updates/s",
                 "h2d_bytes_per_step": wl.input_bytes() * N, "d2h_bytes_per_step": 48 * N,
                 "ms_per_step": statistics.mean(step_e),
-                "path": "paper_2502_16577_b200.permanent(host matrix, workers=N): H2D of the "
-                        "inputs, the walk over N GPUs (one host thread each), D2H of the "
-                        "partials, host combination"},
+                "path": e2e_path},
         "gpu_launches": int(sum(g[0] for g in g_launch)),
         "clocks": clocks.summary(),
     }

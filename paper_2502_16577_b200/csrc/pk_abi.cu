@@ -379,17 +379,30 @@ int dispatch_c128_pair(int n, const pk::C128Launch& a) {
 // Complex register kernel for order n: K3 (one thread per chunk) up to
 // kC128NMax, the lane-pair kernel K3p above (PK_C128_PAIR=1 selects K3p for
 // every order, for A/B runs).
-// K3's fast product schedule: 2 one chain (default), 0 two chains (TC), 1
-// one chain with the fused last multiply (FA). Measured at n = 24..36
-// (profiles/r02_c128_variants.txt): TC -1..-8 %, FA within 1 % of the
-// default. PK_C128_VARIANT overrides it for A/B runs.
+// K1's fast body schedule (PK_DENSE_VARIANT, A/B runs): 0 step-major
+// (default), 1 row-major (pk_dense_f64_launch.cuh)
+int dense_variant() {
+  static const int v = [] {
+    const char* e = getenv("PK_DENSE_VARIANT");
+    return (e && atoi(e) == 1) ? 1 : 0;
+  }();
+  return v;
+}
+
+// K3's fast body schedule (PK_C128_VARIANT, A/B runs): 4 row-major bodies
+// of twice the exact mode's length (default), 2 the step-major bodies of
+// round 1 (profiles/r02_c128_variants*.txt)
 int c128_variant() {
   static const int v = [] {
     const char* e = getenv("PK_C128_VARIANT");
-    const int r = e ? atoi(e) : 2;
-    return (r >= 0 && r <= 2) ? r : 2;
+    return (e && atoi(e) == 2) ? 2 : 4;
   }();
   return v;
+}
+
+// body length (log2) of K3's launch for order n, exact or fast
+int c128_kernel_logu(int n, bool exact) {
+  return exact || c128_variant() == 2 ? pk::c128_logu(n) : pk::c128_fast_logu(n);
 }
 
 bool c128_use_pair(int n) {
@@ -570,6 +583,7 @@ Kind dense_f64_kind(const double* cols, const double* x0, int n, int policy, boo
     pk::DenseLaunch a{};
     a.cols = h_cols;
     a.x0 = h_x0;
+    a.variant = dense_variant();
     a.policy = policy;
     a.exact = exact;
     a.k = k;
@@ -629,7 +643,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   kd.streams = 2;
   const bool pair = c128_use_pair(n);
   kd.logu = pair ? pk::c128_pair_logu(n)
-                 : (n >= pk::kC128NMin && n <= pk::kC128NMax) ? pk::c128_logu(n) : 0;
+                 : (n >= pk::kC128NMin && n <= pk::kC128NMax) ? c128_kernel_logu(n, exact) : 0;
   kd.chunks_log2 = 19;
   const size_t nc = 2 * ncols_of(n);
   // fast modes walk the input rounded onto per-row, per-component grids
@@ -649,6 +663,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
     // (interleaved re, im) appended to the inputs
     auto sp = std::make_shared<pk::SpaC128Spec>(spa_c128_spec(cols, n, exact));
     sp->variant = c128_variant();
+    sp->logu = kd.logu;  // the dense kernel's body length: same fold grouping, same bits
     const size_t voff = kd.input.size();
     for (int j = 0; j < n - 1; ++j)
       for (int r : sp->rows[j]) {
@@ -1547,7 +1562,8 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
     ck(cudaEventRecord(c.e0, c.stream), "event record");
     int k = 0;
     if (n >= pk::kC128NMin) {
-      k = pk::batch_log2_chunk(n, pk::c128_logu(n));
+      k = pk::batch_log2_chunk(n, (flags & PK_FLAG_EXACT) ? pk::c128_logu(n)
+                                                          : pk::c128_fast_logu(n));
       const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
       ensure(c.groups, c.groups_cap, 2 * groups * batch);
       pk::C128BatchLaunch a{};

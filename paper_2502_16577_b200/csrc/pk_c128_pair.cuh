@@ -316,6 +316,74 @@ struct PairFastSteps<N, C, U, U> {
   __device__ __forceinline__ static void run(C128PairFast<N, C>&, double, int) {}
 };
 
+// one body of the fast schedule, row-major (C::RM, as K3's c128_body_rm):
+// each lane forms the U states of its rows one after the other and advances
+// U independent half products; then per step, in order, the shuffle and the
+// combine-and-sum. Same arithmetic and order as the step-major body.
+template <int N, class C>
+__device__ __forceinline__ void pair_body_rm(C128PairFast<N, C>& w, double s_mid, int jz, int jd,
+                                             double sd, bool okd) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  constexpr int H = pair_rows<N>();
+  constexpr int CS = pair_col_stride<N>();
+  const double2* cb = reinterpret_cast<const double2*>(w.scols) + w.half * H;
+  double pr[U], pi[U];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double vr = w.xr[i], vi = w.xi[i];
+#pragma unroll
+    for (int q = 1; q <= U; ++q) {
+      if (q < U) {
+        const int J = ctz_c(q);
+        const double2 v = cb[(J + jz) * CS + i];
+        if (J + 1 < LOGU) {
+          if (((q >> (J + 1)) & 1) == 0) {
+            vr = __dadd_rn(vr, v.x);
+            vi = __dadd_rn(vi, v.y);
+          } else {
+            vr = __dsub_rn(vr, v.x);
+            vi = __dsub_rn(vi, v.y);
+          }
+        } else {
+          vr = __fma_rn(s_mid, v.x, vr);
+          vi = __fma_rn(s_mid, v.y, vi);
+        }
+      } else {
+        const double2 v = cb[jd * CS + i];
+        vr = __fma_rn(sd, v.x, vr);
+        vi = __fma_rn(sd, v.y, vi);
+      }
+      if (i == 0) {
+        pr[q - 1] = vr;
+        pi[q - 1] = vi;
+      } else {
+        const double r = __fma_rn(pr[q - 1], vr, -__dmul_rn(pi[q - 1], vi));
+        const double m = __fma_rn(pr[q - 1], vi, __dmul_rn(pi[q - 1], vr));
+        pr[q - 1] = r;
+        pi[q - 1] = m;
+      }
+    }
+    w.xr[i] = vr;
+    w.xi[i] = vi;
+  }
+#pragma unroll
+  for (int q = 1; q <= U; ++q) {
+    double ar = __shfl_xor_sync(0xffffffffu, pr[q - 1], 1);
+    double ai = __shfl_xor_sync(0xffffffffu, pi[q - 1], 1);
+    if (q & 1) {
+      ar = -ar;
+      ai = -ai;
+    }
+    const double r0 = q == 1 ? 0.0 : w.br, i0 = q == 1 ? 0.0 : w.bi;
+    const double nr = __fma_rn(ar, pr[q - 1], __fma_rn(-ai, pi[q - 1], r0));
+    const double ni = __fma_rn(ar, pi[q - 1], __fma_rn(ai, pr[q - 1], i0));
+    const bool valid = q < U || okd;
+    w.br = valid ? nr : w.br;
+    w.bi = valid ? ni : w.bi;
+  }
+}
+
 template <int N, class C>
 __device__ __forceinline__ dd_t pair_walk_chunk_fast(const double* x0, int k, uint64_t g_end,
                                                      const double* scols, uint64_t c,
@@ -349,15 +417,19 @@ __device__ __forceinline__ dd_t pair_walk_chunk_fast(const double* x0, int k, ui
     const uint64_t gb = base + (m << LOGU);
     const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
     const int jz = (int)(m >> 62);
-    PairFastSteps<N, C, 1, U>::run(w, s_mid, jz);
     // step U: iterate gb + U flips column ctz(gb + U); the lanes of a warp
     // walk different chunks, so the walk's clipped last step is predicated
     // (s = 0 leaves x unchanged) rather than branched around the shuffle
     const uint64_t g = gb + U;
     const bool ok = (m + 1 < nbody) || g <= g_end;
     const int j = ok ? changed_col(g) : 0;
-    w.update(j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0);
-    w.fold(false, false, ok);
+    if constexpr (C::RM) {
+      pair_body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+    } else {
+      PairFastSteps<N, C, 1, U>::run(w, s_mid, jz);
+      w.update(j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0);
+      w.fold(false, false, ok);
+    }
     if (half) w.acc.add(w.br, w.bi);
   }
   if (!half) return dd_t{0.0, 0.0};

@@ -39,8 +39,12 @@ int launch_c128_pair(const C128Launch& a) {
   static_assert(N >= kC128NMin && N <= kDenseNMax, "order out of range");
   constexpr int LOGU = c128_pair_logu(N);
   constexpr int BLK = c128_pair_block(N), MB = c128_pair_minb(N);
-  return a.exact ? launch_c128_pair_cfg<N, C128Cfg<LOGU, true, MB, false, BLK>>(a)
-                 : launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK>>(a);
+  if (a.exact) return launch_c128_pair_cfg<N, C128Cfg<LOGU, true, MB, false, BLK>>(a);
+  // row-major bodies (C128Cfg::RM, +1..4 %, profiles/r02_c128_variants_rm.txt);
+  // PK_C128_VARIANT=2 selects the step-major body, as for K3
+  return a.variant == 2
+             ? launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK>>(a)
+             : launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK, false, true>>(a);
 }
 
 }  // namespace pk

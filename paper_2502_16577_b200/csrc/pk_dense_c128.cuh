@@ -44,13 +44,20 @@ struct DenseC128Params {
 // and the odd rows, and four DFMAs multiply them into the body sum -- the
 // same FP64 instruction count as FA, twice the independent work per term
 // (the single chain is latency bound at 2 warps per scheduler)
+// RM (fast mode): the body is walked row-major -- for each row i the U
+// states of the body are formed one after the other (x_i +- c_{j_q,i}, the
+// same roundings as the step-major walk) and each multiplies its term's
+// running product. The U product chains are independent, the state needs no
+// copies, and each distinct column entry is loaded once per row: same
+// arithmetic, same bits as the step-major schedule, U-fold product ILP.
 template <int LOGU_, bool EXACT_, int MINB_, bool FA_ = false, int BLOCK_ = kC128Block,
-          bool TC_ = false>
+          bool TC_ = false, bool RM_ = false>
 struct C128Cfg {
   static constexpr int LOGU = LOGU_, MINB = MINB_, BLOCK = BLOCK_;
   static constexpr bool EXACT = EXACT_;
   static constexpr bool TC = TC_ && !EXACT_;
-  static constexpr bool FA = FA_ && !EXACT_ && !TC;
+  static constexpr bool RM = RM_ && !EXACT_;
+  static constexpr bool FA = FA_ && !EXACT_ && !TC && !RM;
 };
 
 // complex partial sum: plain (reference) or compensated per component
@@ -237,6 +244,70 @@ struct C128Steps<N, C, U, U> {
   __device__ __forceinline__ static void run(C128Walk<N, C>&, double, int) {}
 };
 
+// one body of U steps, row-major (C::RM): steps 1..U-1 static (column ctz(q),
+// direction from q or s_mid), step U the run-time column jd with direction sd
+// (sd = 0 and no fold when the walk's last step is clipped)
+template <int N, class C>
+__device__ __forceinline__ void c128_body_rm(C128Walk<N, C>& w, double s_mid, int jz, int jd,
+                                             double sd, bool okd) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  const double2* cb = reinterpret_cast<const double2*>(w.scols);
+  double pr[U], pi[U];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double vr = w.xr[i], vi = w.xi[i];
+#pragma unroll
+    for (int q = 1; q <= U; ++q) {
+      if (q < U) {
+        const int J = ctz_c(q);
+        const double2 v = cb[(J + jz) * N + i];
+        if (J + 1 < LOGU) {
+          if (((q >> (J + 1)) & 1) == 0) {
+            vr = __dadd_rn(vr, v.x);
+            vi = __dadd_rn(vi, v.y);
+          } else {
+            vr = __dsub_rn(vr, v.x);
+            vi = __dsub_rn(vi, v.y);
+          }
+        } else {
+          vr = __fma_rn(s_mid, v.x, vr);
+          vi = __fma_rn(s_mid, v.y, vi);
+        }
+      } else {
+        const double2 v = cb[jd * N + i];
+        vr = __fma_rn(sd, v.x, vr);
+        vi = __fma_rn(sd, v.y, vi);
+      }
+      if (i == 0) {
+        pr[q - 1] = vr;
+        pi[q - 1] = vi;
+      } else {
+        const double r = __fma_rn(pr[q - 1], vr, -__dmul_rn(pi[q - 1], vi));
+        const double m = __fma_rn(pr[q - 1], vi, __dmul_rn(pi[q - 1], vr));
+        pr[q - 1] = r;
+        pi[q - 1] = m;
+      }
+    }
+    w.xr[i] = vr;
+    w.xi[i] = vi;
+  }
+  // fold the terms in step order, exactly as the step-major fold()
+#pragma unroll
+  for (int q = 1; q <= U; ++q) {
+    if (q == U && !okd) break;
+    const bool odd = (q & 1) != 0;
+    if (q == 1) {
+      w.br = odd ? -pr[0] : pr[0];
+      w.bi = odd ? -pi[0] : pi[0];
+    } else {
+      w.br = odd ? __dsub_rn(w.br, pr[q - 1]) : __dadd_rn(w.br, pr[q - 1]);
+      w.bi = odd ? __dsub_rn(w.bi, pi[q - 1]) : __dadd_rn(w.bi, pi[q - 1]);
+    }
+  }
+  w.end_body();
+}
+
 template <int N, class C>
 __device__ __forceinline__ dd_t c128_walk_chunk(const double* x0, int k, uint64_t g_end,
                                                 const double* scols, uint64_t c) {
@@ -268,8 +339,14 @@ __device__ __forceinline__ dd_t c128_walk_chunk(const double* x0, int k, uint64_
     const uint64_t gb = base + (m << LOGU);
     const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
     const int jz = (int)(m >> 62);
-    C128Steps<N, C, 1, U>::run(w, s_mid, jz);
     const uint64_t g = gb + U;
+    if constexpr (C::RM) {
+      const bool ok = (m + 1 < nbody) || g <= g_end;
+      const int j = ok ? changed_col(g) : 0;
+      c128_body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+      continue;
+    }
+    C128Steps<N, C, 1, U>::run(w, s_mid, jz);
     if (m + 1 < nbody || g <= g_end) {
       const int j = changed_col(g);
       w.update(scols + 2 * j * N, flip_on(g, j) ? 1.0 : -1.0);

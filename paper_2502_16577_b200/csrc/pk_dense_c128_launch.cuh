@@ -41,16 +41,15 @@ int launch_dense_c128(const C128Launch& a) {
   // fast mode: one 256-thread block per SM to n = 32 (+5 %,
   // profiles/r01_c128_sweep5_blocks.txt); the tail tree has a fixed leaf
   // count (pk_reduce.cuh kTreeLeaves), so results do not depend on it.
-  // a.variant: 2 one chain (default), 0 two product chains (TC), 1 one chain
-  // with the fused last multiply (FA) -- pk_abi.cu c128_variant
+  // a.variant (pk_abi.cu c128_variant): 4 row-major bodies of 2^(LOGU+1)
+  // steps (default), 2 the round-1 step-major bodies of 2^LOGU (A/B runs;
+  // two product chains, the fused last multiply and other body lengths were
+  // measured slower, profiles/r02_c128_variants*.txt)
   constexpr int FB = N <= 32 ? 256 : kC128Block;
   constexpr int FM = N <= 32 ? 1 : MB;
   if (a.exact) return launch_c128_cfg<N, C128Cfg<LOGU, true, MB>>(a, p);
-  switch (a.variant) {
-    case 1: return launch_c128_cfg<N, C128Cfg<LOGU, false, FM, true, FB>>(a, p);
-    case 0: return launch_c128_cfg<N, C128Cfg<LOGU, false, FM, false, FB, true>>(a, p);
-    default: return launch_c128_cfg<N, C128Cfg<LOGU, false, FM, false, FB>>(a, p);
-  }
+  if (a.variant == 2) return launch_c128_cfg<N, C128Cfg<LOGU, false, FM, false, FB>>(a, p);
+  return launch_c128_cfg<N, C128Cfg<c128_fast_logu(N), false, FM, false, FB, false, true>>(a, p);
 }
 
 template <int N, class C>
@@ -77,10 +76,11 @@ template <int N>
 int launch_dense_c128_batch(const C128BatchLaunch& a) {
   constexpr int LOGU = c128_logu(N);
   constexpr int MB = c128_minb(N);
-  // fast: the single launch's default schedule, so a batch entry and a
-  // single walk of the same matrix agree bit for bit
+  // fast: the single launch's default body (row-major, 2^(LOGU+1) steps),
+  // so a batch entry and a single walk of the same matrix agree bit for bit
   return a.exact ? launch_c128_batch_cfg<N, C128Cfg<LOGU, true, MB>>(a)
-                 : launch_c128_batch_cfg<N, C128Cfg<LOGU, false, MB>>(a);
+                 : launch_c128_batch_cfg<N, C128Cfg<c128_fast_logu(N), false, MB, false,
+                                                    kC128Block, false, true>>(a);
 }
 
 }  // namespace pk

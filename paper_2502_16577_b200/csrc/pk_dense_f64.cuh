@@ -83,14 +83,21 @@ __device__ __forceinline__ double row_product(const double (&x)[N]) {
 //        the body's terms are summed with a two_sum on the hi parts plus a
 //        plain sum of the lo parts and folded once per body into the
 //        double-double partial
+//   RM   row-major body (with FA): for each row the U states of the body are
+//        formed one after the other -- the same additions in the same order
+//        as the step-major walk -- and multiply the U independent running
+//        products; the last row's multiply folds into the body sum in step
+//        order. Same bits as the step-major body, U independent chains, no
+//        state copies, each distinct column entry loaded once per row
 template <int POL_, int PS_, int LOGU_, bool BA_, int MINB_ = 1, int BLOCK_ = 128,
-          bool FA_ = false, bool QF_ = false>
+          bool FA_ = false, bool QF_ = false, bool RM_ = false>
 struct DenseCfg {
   static constexpr int POL = POL_, PS = PS_, LOGU = LOGU_, MINB = MINB_;
   static constexpr int BLOCK = BLOCK_;
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
   static constexpr bool FA = FA_ && BA;
   static constexpr bool QF = QF_ && POL_ == POL_QQ;
+  static constexpr bool RM = RM_ && FA;
 };
 
 template <int N>
@@ -239,6 +246,45 @@ struct StaticSteps<N, C, U, U> {
   __device__ __forceinline__ static void run(DenseWalk<N, C>&, double, int) {}
 };
 
+// One body, row-major (C::RM): static steps q < U (column ctz(q), direction
+// from q or s_mid), step U the run-time column jd with direction sd (sd = 0
+// and no fold when the walk's last step is clipped).
+template <int N, class C>
+__device__ __forceinline__ void body_rm(DenseWalk<N, C>& w, double s_mid, int jz, int jd,
+                                        double sd, bool okd) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  constexpr int NP = smem_stride<N>();
+  const double* cb = w.scols;
+  double p[U];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = w.x[i];
+#pragma unroll
+    for (int q = 1; q <= U; ++q) {
+      if (q < U) {
+        const int J = ctz_c(q);
+        const double c = cb[(J + jz) * NP + i];
+        if (J + 1 < LOGU) v = (((q >> (J + 1)) & 1) == 0) ? __dadd_rn(v, c) : __dsub_rn(v, c);
+        else v = __fma_rn(s_mid, c, v);
+      } else {
+        v = __fma_rn(sd, cb[jd * NP + i], v);
+      }
+      if (i == 0) {
+        p[q - 1] = v;
+      } else if (i < N - 1) {
+        p[q - 1] = __dmul_rn(p[q - 1], v);
+      } else if (q < U || okd) {
+        // FA: the last multiply fused with the body sum, in step order
+        const double sp = (q & 1) ? -p[q - 1] : p[q - 1];
+        w.bsum = q == 1 ? __dmul_rn(sp, v) : __fma_rn(sp, v, w.bsum);
+      }
+    }
+    w.x[i] = v;
+  }
+  w.end_body();
+}
+
 // Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
 // g_end) incrementally from its jump-in state, like run_range; returns its
 // normalised partial (parallel.py:282-289). In the fast modes the host has
@@ -258,9 +304,15 @@ __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0
     const uint64_t gb = base + (m << LOGU);
     const double s_mid = flip_on(gb + (U >> 1), LOGU - 1) ? 1.0 : -1.0;
     const int jz = (int)(m >> 62);  // always 0 (m < 2^62) but opaque to ptxas
-    StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
     // step U of the body: iterate gb + U flips column ctz(gb + U) >= LOGU
     const uint64_t g = gb + U;
+    if constexpr (C::RM) {
+      const bool ok = (m + 1 < nbody) || g <= g_end;
+      const int j = ok ? changed_col(g) : 0;
+      body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+      continue;
+    }
+    StaticSteps<N, C, 1, U>::run(w, s_mid, jz);
     if (m + 1 < nbody || g <= g_end) {
       const int j = changed_col(g);
       w.update_dynamic(j, flip_on(g, j) ? 1.0 : -1.0);

@@ -46,8 +46,13 @@ int launch_dense_f64(const DenseLaunch& a) {
       return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_KAHAN:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a, p);
+      // a.variant (PK_DENSE_VARIANT, A/B runs): 0 step-major body (default),
+      // 1 row-major body -- same bits, within 1 % (profiles/r02_k1_variants.txt;
+      // 384-thread row-major blocks and 32-step bodies were no better)
+      if (a.variant == 1)
+        return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
+      return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_DQ:
       return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);

@@ -75,6 +75,7 @@ struct DenseLaunch {
   unsigned int* counter;
   cudaStream_t stream;
   int sms;
+  int variant;          // fast-mode body schedule (pk_dense_f64_launch.cuh)
 };
 
 // Launches the N-specialised register kernel; returns cudaError_t.
@@ -128,6 +129,9 @@ constexpr int kC128NMax = 40;
 // complex state is 4N registers; longer bodies make ptxas interleave more
 // product chains than the register file holds, so bodies stay short
 constexpr int c128_logu(int N) { return N <= 32 ? 2 : 1; }
+// fast mode walks row-major bodies of twice that length (C128Cfg::RM):
+// +3..6 % at n = 28..36 (profiles/r02_c128_variants_rm.txt)
+constexpr int c128_fast_logu(int N) { return c128_logu(N) + 1; }
 constexpr int c128_minb(int N) { return N <= 32 ? 2 : 1; }
 
 struct C128Launch {

@@ -84,6 +84,7 @@ struct SpaC128Spec {
   std::vector<std::vector<int>> rows;  // nonzero rows of column j < n-1
   bool exact = false;
   int variant = 0;  // fast-mode product schedule, as K3's C128Launch::variant
+  int logu = 0;     // body length (log2); 0: spa_c128_logu(n)
 };
 
 struct SpaC128Launch {

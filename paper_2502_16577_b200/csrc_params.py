@@ -18,6 +18,11 @@ def c128_logu(n: int) -> int:
     return 2 if n <= 32 else 1
 
 
+def c128_fast_logu(n: int) -> int:
+    """K3's fast (row-major) body length: twice the exact mode's."""
+    return c128_logu(n) + 1
+
+
 def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:
     """pk_abi.cu plan_dense's automatic chunk exponent for a range whose
     length has `bit_len` bits (a whole walk: n - 1)."""
@@ -36,5 +41,5 @@ def c128_pair_logu(n: int) -> int:
 
 
 def c128_register_logu(n: int) -> int:
-    """Body length exponent of the complex register kernel the library runs at order n."""
-    return c128_logu(n) if n <= C128_N_MAX else c128_pair_logu(n)
+    """Body length exponent of the fast complex register kernel at order n."""
+    return c128_fast_logu(n) if n <= C128_N_MAX else c128_pair_logu(n)

@@ -69,10 +69,10 @@ def test_complex_batch_equals_single_launch_bitwise(n, exact):
     # one launch for many Haar submatrices (boson sampling) must give each
     # matrix exactly what pk_dense_c128 gives with the same chunk exponent
     from paper_2502_16577_b200.complex_walk import DenseC128Problem
-    from paper_2502_16577_b200.csrc_params import c128_logu
+    from paper_2502_16577_b200.csrc_params import c128_fast_logu, c128_logu
     ms = [pk.haar_unitary_block(n, 40 + s) for s in range(5)]
     got = pk.permanent_batch(ms, exact=exact)
-    k = batch_log2_chunk(n, c128_logu(n))
+    k = batch_log2_chunk(n, c128_logu(n) if exact else c128_fast_logu(n))
     for m, g in zip(ms, got):
         prob = DenseC128Problem(m)
         wr, wi = prob.walk(1, pk.total_iterates(n), exact=exact, log2_chunk=k)

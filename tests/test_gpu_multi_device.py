@@ -24,7 +24,10 @@ def _mats():
 
 
 def two_devices():
-    return _native.device_count() >= 2
+    try:  # evaluated at collection, also on CPU-only hosts
+        return _native.device_count() >= 2
+    except Exception:
+        return False
 
 
 @pytest.mark.parametrize("kind,m,policy", _mats())
