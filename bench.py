@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--range-log2", type=int, default=0,
                     help="profiling aid: walk only iterates [1, 2^x] (same kernels)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the other BASELINE workloads' short measurements (N=1 only)")
     ap.add_argument("--cpu-sample-log2", type=int, default=31,
                     help="iterates of the n-walk timed for the CPU baseline (2^x)")
     return ap.parse_args()
@@ -429,7 +431,7 @@ class Workload:
 # ncu --set full summaries of each workload's dominant kernel (profiles/):
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch
 NCU_SUMMARY = {"dense": "r02_ncu_k1_full_summary.csv", "sparse": "r02_ncu_spa_f64_full_summary.csv",
-               "haar": "r01_ncu_k3_full_summary.csv", "binary": "r01_ncu_k6_full_summary.csv"}
+               "haar": "r02_ncu_k3_full_summary.csv", "binary": "r01_ncu_k6_full_summary.csv"}
 
 
 def ncu_metric(kind, metric):
@@ -633,8 +635,49 @@ def run_b200(args, dist: Dist):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if N == 1 and not args.no_extra and not args.range_log2 and wl.kind == "dense":
+        line["other_workloads"] = other_workloads(args, dev)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def other_workloads(args, dev):
+    """Short measurements of the other BASELINE configurations on the same
+    box (config 2: dense n=36; config 3: binary n=40 exact; config 4: Haar
+    n=32 complex; the SpaRyser real kernel at n=40; the lane-pair complex
+    kernel at n=48 on a 2^38-iterate sample), whole walks unless stated: 1
+    untimed + 2 timed steps each, kernel CUDA-event time, L2 flushed."""
+    out = []
+    flusher = L2Flusher(dev[0])
+    for kind, n, sample in (("dense", 36, 0), ("binary", 40, 0), ("haar", 32, 0),
+                            ("sparse", 40, 0), ("haar", 48, 38)):
+        a = argparse.Namespace(**vars(args))
+        a.workload, a.n, a.range_log2 = kind, n, sample
+        try:
+            wl = Workload(a)
+            wl.range_sample = bool(sample)
+            total = (1 << (n - 1)) - 1 if not sample else (1 << sample)
+            wl.walk(1, total, dev)
+            ms = []
+            for _ in range(2):
+                flusher.flush()
+                sync_device()
+                part, st = wl.walk(1, total, dev)
+                sync_device()
+                ms.append(st.kernel_ms)
+            ups = total / (statistics.mean(ms) * 1e-3)
+            rec = {"workload": wl.desc if not sample else
+                   f"{wl.desc.split(',')[0]}, iterates [1, 2^{sample}] (sample)",
+                   "n": n, "value": ups, "unit": "updates/s",
+                   "ms_per_step": statistics.mean(ms)}
+            if wl.flops:
+                rec["fp64_tflops"] = ups * wl.flops * 1e-12
+            if not sample:
+                rec["permanent"] = wl.combine([part])
+            out.append(rec)
+        except Exception as exc:  # reported, not fatal: the headline line stands
+            out.append({"workload": f"{kind} n={n}", "error": repr(exc)[:200]})
+    return out
 
 
 def main():
