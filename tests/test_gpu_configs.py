@@ -246,3 +246,18 @@ def test_config3_binary40_two_independent_kernels_agree():
     a = int_walk_total(m, sparse=True)
     b = int_walk_total(m, sparse=False)
     assert a == b == 48153712130998394697054824
+
+
+def test_config5_n48_fast_vs_precise_on_a_range():
+    # config 5's matrix: a whole n = 48 walk in precise mode would take hours,
+    # so the fast walk (exact states) is checked against it on the first 2^38
+    # iterates (1/512 of the walk), every policy
+    m = pk.random_real(48, 20261017, 0.0, 1.0)
+    prob = DenseF64Problem(m)
+    hi = 1 << 38
+    want = prob.walk(1, hi, AccumulatorPolicy.KAHAN, precise=True)
+    w = want.hi + want.lo
+    for pol in ("kahan", "dq", "qq"):
+        got = prob.walk(1, hi, AccumulatorPolicy.parse(pol))
+        g = got.hi + got.lo
+        assert abs(g - w) <= 1e-10 * abs(w), (pol, g, w, (g - w) / w)
