@@ -157,7 +157,8 @@ int pk_spa_f64_source(const double* cols, int n, int policy, uint32_t flags, cha
  * chunk and reduce each component as a double-double tree.
  *
  * pk_dense_c128: out = (re_hi, re_lo, im_hi, im_lo) over [start, end]
- * (register kernels for 11 <= n <= 40, range walkers otherwise).
+ * (register kernels for 11 <= n <= 63 -- one thread per chunk to n = 40,
+ * a lane pair per chunk above -- range walkers otherwise).
  * pk_dense_c128_ranges: bit-identical run_range partials, out = (re, im) per
  * range (chunk_dense_c128, _loops.py:186-209).
  * pk_dense_c128_chunks: per-chunk (re, im) partials, out_total as above. */
@@ -170,7 +171,7 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
                          uint64_t chunk_lo, uint64_t nchunks, uint32_t flags, int device,
                          double* out_chunks, double out_total[4]);
 
-/* Whole complex walks of `batch` matrices of one order n <= 40 in one launch
+/* Whole complex walks of `batch` matrices of one order n <= 63 in one launch
  * (boson-sampling submatrices). cols/x0 back to back in the
  * pk_dense_c128 layout; out[4*b .. 4*b+3] = (re_hi, re_lo, im_hi, im_lo) of
  * matrix b's partial over [1, 2^(n-1)-1] (add the g = 0 product and the

@@ -4,7 +4,7 @@ permkit evaluates decomposition leaves one by one (preprocess.py:495-504),
 and boson-sampling workloads need the permanents of many n ~ 20-30
 submatrices. ``permanent_batch`` groups the matrices by kind and order and
 walks every real group in ONE launch of ``pk_dense_f64_batch`` and every
-complex group of order <= 40 in ONE launch of ``pk_dense_c128_batch`` and
+complex group of order <= 63 in ONE launch of ``pk_dense_c128_batch`` and
 every integer group in ONE launch of ``pk_int_batch`` (one block per matrix
 at a time, each matrix's aligned chunks reduced exactly like a single
 launch). Complex orders above 40 take one device call per matrix (still on
@@ -72,7 +72,7 @@ def real_batch_arrays(A: np.ndarray, policy: AccumulatorPolicy, device: int = 0,
 
 def complex_batch_arrays(A: np.ndarray, device: int = 0, exact: bool = False,
                          stats: Optional[nat.RunStats] = None) -> List[complex]:
-    """Permanents of the complex matrices A[b, n, n] (n <= 40) in one
+    """Permanents of the complex matrices A[b, n, n] (n <= 63) in one
     pk_dense_c128_batch launch."""
     b, n, _ = A.shape
     cols, x0 = dense_states(np.asarray(A, dtype=np.complex128))
@@ -127,7 +127,7 @@ def permanent_batch(matrices, policy="dd", *, device: int = 0, exact: bool = Fal
             ds = [sparse_to_dense(ms[i]) if isinstance(ms[i], SparsePair) else ms[i] for i in idx]
             for i, v in zip(idx, int_batch_totals(ds, device, stats)):
                 out[i] = v
-        elif kind == KIND_COMPLEX and n <= 40:
+        elif kind == KIND_COMPLEX and n <= 63:
             if policy is not AccumulatorPolicy.DD:
                 from .errors import PolicyError
                 raise PolicyError("complex matrices support the plain-double policy only")

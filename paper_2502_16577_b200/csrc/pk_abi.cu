@@ -376,6 +376,25 @@ int dispatch_c128_pair(int n, const pk::C128Launch& a) {
   }
 }
 
+int dispatch_c128_pair_batch(int n, const pk::C128BatchLaunch& a) {
+  switch (n) {
+#define PK_CASE(N) \
+  case N:          \
+    return pk::launch_c128_pair_batch<N>(a);
+    PK_CASE(11) PK_CASE(12) PK_CASE(13) PK_CASE(14) PK_CASE(15) PK_CASE(16) PK_CASE(17)
+    PK_CASE(18) PK_CASE(19) PK_CASE(20) PK_CASE(21) PK_CASE(22) PK_CASE(23) PK_CASE(24)
+    PK_CASE(25) PK_CASE(26) PK_CASE(27) PK_CASE(28) PK_CASE(29) PK_CASE(30) PK_CASE(31)
+    PK_CASE(32) PK_CASE(33) PK_CASE(34) PK_CASE(35) PK_CASE(36) PK_CASE(37) PK_CASE(38)
+    PK_CASE(39) PK_CASE(40) PK_CASE(41) PK_CASE(42) PK_CASE(43) PK_CASE(44) PK_CASE(45) PK_CASE(46) PK_CASE(47)
+    PK_CASE(48) PK_CASE(49) PK_CASE(50) PK_CASE(51) PK_CASE(52) PK_CASE(53) PK_CASE(54)
+    PK_CASE(55) PK_CASE(56) PK_CASE(57) PK_CASE(58) PK_CASE(59) PK_CASE(60) PK_CASE(61)
+    PK_CASE(62) PK_CASE(63)
+#undef PK_CASE
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
 // Complex register kernel for order n: K3 (one thread per chunk) up to
 // kC128NMax, the lane-pair kernel K3p above (PK_C128_PAIR=1 selects K3p for
 // every order, for A/B runs).
@@ -1536,7 +1555,6 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
     if (batch < 0) fail(PK_ERR_ARG, "negative batch");
     if (batch == 0) return;
     if (!x0 || !out || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
-    if (n > pk::kC128NMax) fail(PK_ERR_ARG, "batched complex walks need n <= 40");
     const size_t ncol = 2 * (size_t)(n > 1 ? n - 1 : 0) * n;
     DevCtx& c = dev_ctx(device);
     std::lock_guard<std::mutex> lock(c.mu);
@@ -1562,8 +1580,10 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
     ck(cudaEventRecord(c.e0, c.stream), "event record");
     int k = 0;
     if (n >= pk::kC128NMin) {
-      k = pk::batch_log2_chunk(n, (flags & PK_FLAG_EXACT) ? pk::c128_logu(n)
-                                                          : pk::c128_fast_logu(n));
+      const bool pair = c128_use_pair(n);  // K3p above K3's register limit
+      k = pk::batch_log2_chunk(n, pair ? pk::c128_pair_logu(n)
+                                  : (flags & PK_FLAG_EXACT) ? pk::c128_logu(n)
+                                                            : pk::c128_fast_logu(n));
       const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);
       ensure(c.groups, c.groups_cap, 2 * groups * batch);
       pk::C128BatchLaunch a{};
@@ -1576,7 +1596,8 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
       a.out = c.chunks;
       a.stream = c.stream;
       a.sms = c.sms;
-      ck((cudaError_t)dispatch_c128_batch(n, a), "dense_c128 batch launch");
+      ck((cudaError_t)(pair ? dispatch_c128_pair_batch(n, a) : dispatch_c128_batch(n, a)),
+         "dense_c128 batch launch");
     } else {
       const unsigned grid = (unsigned)((batch + pk::kWalkBlock - 1) / pk::kWalkBlock);
       pk::walk_dense_c128_multi<<<grid, pk::kWalkBlock, 0, c.stream>>>(d_cols, d_x0, n, batch, c.chunks);

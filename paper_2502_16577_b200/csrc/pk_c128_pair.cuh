@@ -495,4 +495,52 @@ __global__ void __launch_bounds__(C::BLOCK, C::MINB)
   grid_tail_reduce_pairs<C::BLOCK>(p.group_part, p.num_groups, p.out, p.counter);
 }
 
+// batched whole walks (boson-sampling submatrices, decomposition leaves) of
+// order 41..63: one block per matrix at a time, its 2^(N-1-k) aligned chunks
+// walked by the block's warps in the single launch's lane-pair layout and
+// folded with the same trees, so a batch entry equals the single walk of the
+// same chunk exponent bit for bit (as dense_c128_batch does for K3)
+template <int N, class C>
+__global__ void __launch_bounds__(C::BLOCK, C::MINB)
+    dense_c128_pair_batch(const __grid_constant__ C128BatchParams<N> p) {
+  extern __shared__ __align__(16) double scols[];
+  const double* sx0 = scols + 2 * (N - 1) * pair_col_stride<N>();
+  const uint64_t total = (1ull << (N - 1)) - 1;
+  const int groups = (int)((1ull << (N - 1 - p.k)) / 32);
+  const unsigned int lane = threadIdx.x & 31u;
+  const int half = (int)(lane & 1u);
+  const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    __syncthreads();
+    pair_stage<N>(scols, p.cols + (size_t)b * 2 * (N - 1) * N, p.x0 + (size_t)b * 2 * N);
+    __syncthreads();
+    dd_t* gp = p.group_part + (size_t)b * 2 * groups;
+    for (int grp = wib; grp < groups; grp += wpb) {
+      dd_t part[2];
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const uint64_t c = (uint64_t)grp * 32 + pass * 16 + (lane >> 1);
+        if constexpr (C::EXACT)
+          part[pass] = pair_walk_chunk<N, C>(sx0, p.k, total, scols, c, half);
+        else
+          part[pass] = pair_walk_chunk_fast<N, C>(sx0, p.k, total, scols, c, half);
+      }
+      const int src = 2 * (int)(lane & 15u) + 1;
+      const double r0 = __shfl_sync(0xffffffffu, part[0].hi, src);
+      const double i0 = __shfl_sync(0xffffffffu, part[0].lo, src);
+      const double r1 = __shfl_sync(0xffffffffu, part[1].hi, src);
+      const double i1 = __shfl_sync(0xffffffffu, part[1].lo, src);
+      const dd_t mine = lane < 16 ? dd_t{r0, i0} : dd_t{r1, i1};
+      dd_t re{mine.hi, 0.0}, im{mine.lo, 0.0};
+      warp_tree_cdd(re, im);
+      if (lane == 0) {
+        gp[2 * grp] = re;
+        gp[2 * grp + 1] = im;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) p.out[2 * b + threadIdx.x] = pairwise_fold(gp, 0, groups, 2, threadIdx.x);
+  }
+}
+
 }  // namespace pk

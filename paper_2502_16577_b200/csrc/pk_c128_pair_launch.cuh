@@ -47,6 +47,36 @@ int launch_c128_pair(const C128Launch& a) {
              : launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK, false, true>>(a);
 }
 
+template <int N, class C>
+static int launch_c128_pair_batch_cfg(const C128BatchLaunch& a) {
+  auto kern = dense_c128_pair_batch<N, C>;
+  constexpr size_t smem = pair_smem_bytes<N>();
+  static std::atomic<int> slots[kMaxDevices];  // per device ordinal
+  int occ = 1;
+  if (int rc = prep_kernel(kern, C::BLOCK, smem, slots, &occ)) return rc;
+  C128BatchParams<N> p;
+  p.cols = a.d_cols;
+  p.x0 = a.d_x0;
+  p.group_part = a.group_part;
+  p.out = a.out;
+  p.batch = a.batch;
+  p.k = a.k;
+  uint64_t grid = (uint64_t)a.sms * (uint64_t)occ;
+  if ((uint64_t)a.batch < grid) grid = a.batch;
+  kern<<<(unsigned)grid, C::BLOCK, smem, a.stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+template <int N>
+int launch_c128_pair_batch(const C128BatchLaunch& a) {
+  constexpr int LOGU = c128_pair_logu(N);
+  constexpr int BLK = c128_pair_block(N), MB = c128_pair_minb(N);
+  if (a.exact) return launch_c128_pair_batch_cfg<N, C128Cfg<LOGU, true, MB, false, BLK>>(a);
+  return launch_c128_pair_batch_cfg<N, C128Cfg<LOGU, false, MB, false, BLK, false, true>>(a);
+}
+
 }  // namespace pk
 
-#define PK_INSTANTIATE_C128_PAIR(N) template int pk::launch_c128_pair<N>(const pk::C128Launch&);
+#define PK_INSTANTIATE_C128_PAIR(N)                                    \
+  template int pk::launch_c128_pair<N>(const pk::C128Launch&); \
+  template int pk::launch_c128_pair_batch<N>(const pk::C128BatchLaunch&);

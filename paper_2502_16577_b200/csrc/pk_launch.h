@@ -179,6 +179,10 @@ struct C128BatchLaunch {
 template <int N>
 int launch_dense_c128_batch(const C128BatchLaunch& a);
 
+// batched lane-pair walks, orders above kC128NMax (pk_c128_pair.cuh)
+template <int N>
+int launch_c128_pair_batch(const C128BatchLaunch& a);
+
 // exact integers (pk_int.cuh): z-space state, |z_i| < 2^zb
 constexpr int kIntNMin = 11;
 constexpr int kIntNMax = 63;

@@ -70,3 +70,47 @@ def test_pair_whole_walk_n41_fast_vs_exact():
     im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
     exact = complex(re.hi, im.hi) * pk.kernels._sign_factor(41)
     assert abs(fast - exact) <= 1e-10 * abs(exact), (fast, exact, abs(fast - exact) / abs(exact))
+
+
+PAIR_BATCH_PROBE = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_2502_16577_b200 as pk
+from paper_2502_16577_b200.complex_walk import DenseC128Problem
+from paper_2502_16577_b200.csrc_params import c128_pair_logu
+from paper_2502_16577_b200.kernels import _sign_factor
+from paper_2502_16577_b200.precision import DoubleDouble, dd_add
+n = int(sys.argv[1])
+out = []
+for exact in (False, True):
+    ms = [pk.haar_unitary_block(n, 60 + s, m=2 * n) for s in range(3)]
+    got = pk.permanent_batch(ms, exact=exact)
+    k = max(n - 1 - 10, c128_pair_logu(n) + 1)
+    for m, g in zip(ms, got):
+        prob = DenseC128Problem(m)
+        wr, wi = prob.walk(1, (1 << (n - 1)) - 1, exact=exact, log2_chunk=k)
+        p0 = prob.p0()
+        re = dd_add(DoubleDouble(p0.real, 0.0), wr)
+        im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+        s = _sign_factor(n)
+        out.append([g.real.hex(), g.imag.hex(), (re.hi * s).hex(), (im.hi * s).hex()])
+print(json.dumps(out))
+"""
+
+
+def test_pair_batch_equals_single_launch_bitwise():
+    # batched complex walks above n = 40 run the lane-pair layout, whose
+    # entries must equal the single walk with the batch's chunk exponent bit
+    # for bit. PK_C128_PAIR=1 (read once per process) routes n = 24 through
+    # the same kernels, so the check runs in seconds in a subprocess.
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PK_C128_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", PAIR_BATCH_PROBE % root, "24"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for row in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert row[0:2] == row[2:4], row

@@ -261,3 +261,20 @@ def test_config5_n48_fast_vs_precise_on_a_range():
         got = prob.walk(1, hi, AccumulatorPolicy.parse(pol))
         g = got.hi + got.lo
         assert abs(g - w) <= 1e-10 * abs(w), (pol, g, w, (g - w) / w)
+
+
+def test_config4_haar32_fast_vs_exact_short_chunks():
+    # the exact mode (the reference's incremental row sums) over 2^10-step
+    # chunks barely drifts; the fast walk's states are exact. North-star
+    # tolerance between the two at config 4.
+    from paper_2502_16577_b200.precision import DoubleDouble, dd_add
+    d = load("haar32_dd")
+    m = matrix(d["matrix"])
+    fast = pk.perm_nw(m)
+    prob = DenseC128Problem(m)
+    wr, wi = prob.walk(1, (1 << 31) - 1, exact=True, log2_chunk=10)
+    p0 = prob.p0()
+    re = dd_add(DoubleDouble(p0.real, 0.0), wr)
+    im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+    exact = complex(re.hi, im.hi) * pk.kernels._sign_factor(32)
+    assert abs(fast - exact) <= REL_TOL * abs(exact), (fast, exact, abs(fast - exact) / abs(exact))
