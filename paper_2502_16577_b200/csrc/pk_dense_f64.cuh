@@ -97,7 +97,7 @@ struct DenseCfg {
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
   static constexpr bool FA = FA_ && BA;
   static constexpr bool QF = QF_ && POL_ == POL_QQ;
-  static constexpr bool RM = RM_ && FA;
+  static constexpr bool RM = RM_ && (FA || QF);
 };
 
 template <int N>
@@ -285,6 +285,65 @@ __device__ __forceinline__ void body_rm(DenseWalk<N, C>& w, double s_mid, int jz
   w.end_body();
 }
 
+// Fast QQ body, row-major (C::RM with C::QF): the U double-double products
+// advance row by row, then fold in step order exactly as DenseWalk::fold.
+template <int N, class C>
+__device__ __forceinline__ void body_rm_qf(DenseWalk<N, C>& w, double s_mid, int jz, int jd,
+                                           double sd, bool okd) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  constexpr int NP = smem_stride<N>();
+  const double* cb = w.scols;
+  double hi[U], lo[U];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = w.x[i];
+#pragma unroll
+    for (int q = 1; q <= U; ++q) {
+      if (q < U) {
+        const int J = ctz_c(q);
+        const double c = cb[(J + jz) * NP + i];
+        if (J + 1 < LOGU) v = (((q >> (J + 1)) & 1) == 0) ? __dadd_rn(v, c) : __dsub_rn(v, c);
+        else v = __fma_rn(s_mid, c, v);
+      } else {
+        v = __fma_rn(sd, cb[jd * NP + i], v);
+      }
+      if (i == 0) {
+        hi[q - 1] = v;  // x_0, multiplied at row 1
+      } else if (i == 1) {
+        const double h = __dmul_rn(hi[q - 1], v);
+        lo[q - 1] = __fma_rn(hi[q - 1], v, -h);
+        hi[q - 1] = h;
+      } else {
+        const double h2 = __dmul_rn(hi[q - 1], v);
+        lo[q - 1] = __fma_rn(lo[q - 1], v, __fma_rn(hi[q - 1], v, -h2));
+        hi[q - 1] = h2;
+      }
+    }
+    w.x[i] = v;
+  }
+#pragma unroll
+  for (int q = 1; q <= U; ++q) {
+    if (q == U && !okd) break;
+    double h = hi[q - 1], l = lo[q - 1];
+    if (q & 1) {
+      h = -h;
+      l = -l;
+    }
+    if (q == 1) {
+      w.qs = h;
+      w.qc = 0.0;
+      w.ql = l;
+    } else {
+      double e;
+      two_sum(w.qs, h, w.qs, e);
+      w.qc = __dadd_rn(w.qc, e);
+      w.ql = __dadd_rn(w.ql, l);
+    }
+  }
+  w.end_body();
+}
+
 // Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
 // g_end) incrementally from its jump-in state, like run_range; returns its
 // normalised partial (parallel.py:282-289). In the fast modes the host has
@@ -309,7 +368,10 @@ __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0
     if constexpr (C::RM) {
       const bool ok = (m + 1 < nbody) || g <= g_end;
       const int j = ok ? changed_col(g) : 0;
-      body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+      if constexpr (C::QF)
+        body_rm_qf<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+      else
+        body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
       continue;
     }
     StaticSteps<N, C, 1, U>::run(w, s_mid, jz);

@@ -57,8 +57,13 @@ int launch_dense_f64(const DenseLaunch& a) {
       return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_QQ:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p);
+      // row-major fast QQ (same bits) above n = 36, where the step-major body
+      // spills: +12 % at n = 40, -3..5 % at n = 32..36
+      // (profiles/r02_qq_variants.txt); PK_DENSE_VARIANT=1 forces it
+      if (N > 36 || a.variant == 1)
+        return launch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true, true>>(a, p);
+      return launch_cfg<N, DenseCfg<POL_QQ, 1, qf_logu(N), false, MB, 128, false, true>>(a, p);
     default:
       return (int)cudaErrorInvalidValue;
   }
