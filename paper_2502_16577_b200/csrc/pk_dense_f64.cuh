@@ -97,7 +97,7 @@ struct DenseCfg {
   static constexpr bool BA = BA_ && POL_ != POL_QQ;
   static constexpr bool FA = FA_ && BA;
   static constexpr bool QF = QF_ && POL_ == POL_QQ;
-  static constexpr bool RM = RM_ && (FA || QF);
+  static constexpr bool RM = RM_ && (FA || QF || !BA);
 };
 
 template <int N>
@@ -344,6 +344,55 @@ __device__ __forceinline__ void body_rm_qf(DenseWalk<N, C>& w, double s_mid, int
   w.end_body();
 }
 
+// Per-term policy fold (exact modes: no body sums), row-major: the U
+// products are the reference's sequential chains (prod = x_0 * x_1 ...; QQ
+// from (1, 0) with qq_mul_step, _loops.py:50-87), folded term by term in step
+// order -- bit-identical to the step-major walk and to run_range per chunk.
+template <int N, class C>
+__device__ __forceinline__ void body_rm_exact(DenseWalk<N, C>& w, double s_mid, int jz, int jd,
+                                              double sd, bool okd) {
+  constexpr int LOGU = C::LOGU;
+  constexpr int U = 1 << LOGU;
+  constexpr int NP = smem_stride<N>();
+  constexpr bool QQ = C::POL == POL_QQ;
+  const double* cb = w.scols;
+  double ph[U], pl[U];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = w.x[i];
+#pragma unroll
+    for (int q = 1; q <= U; ++q) {
+      if (q < U) {
+        const int J = ctz_c(q);
+        const double c = cb[(J + jz) * NP + i];
+        if (J + 1 < LOGU) v = (((q >> (J + 1)) & 1) == 0) ? __dadd_rn(v, c) : __dsub_rn(v, c);
+        else v = __fma_rn(s_mid, c, v);
+      } else {
+        v = __fma_rn(sd, cb[jd * NP + i], v);
+      }
+      if constexpr (QQ) {
+        if (i == 0) {
+          ph[q - 1] = 1.0;
+          pl[q - 1] = 0.0;
+        }
+        qq_mul_step(ph[q - 1], pl[q - 1], v);
+      } else {
+        ph[q - 1] = i == 0 ? v : __dmul_rn(ph[q - 1], v);
+      }
+    }
+    w.x[i] = v;
+  }
+#pragma unroll
+  for (int q = 1; q <= U; ++q) {
+    if (q == U && !okd) break;
+    if constexpr (QQ) {
+      if (q & 1) w.acc.sub2(ph[q - 1], pl[q - 1]); else w.acc.add2(ph[q - 1], pl[q - 1]);
+    } else {
+      if (q & 1) w.acc.sub(ph[q - 1]); else w.acc.add(ph[q - 1]);
+    }
+  }
+}
+
 // Walk one aligned chunk c (iterates [1 + c*2^k, (c+1)*2^k], clipped at
 // g_end) incrementally from its jump-in state, like run_range; returns its
 // normalised partial (parallel.py:282-289). In the fast modes the host has
@@ -368,10 +417,10 @@ __device__ __forceinline__ dd_t walk_chunk(const double* scols, const double* x0
     if constexpr (C::RM) {
       const bool ok = (m + 1 < nbody) || g <= g_end;
       const int j = ok ? changed_col(g) : 0;
-      if constexpr (C::QF)
-        body_rm_qf<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
-      else
-        body_rm<N, C>(w, s_mid, jz, j, ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0, ok);
+      const double sd = ok ? (flip_on(g, j) ? 1.0 : -1.0) : 0.0;
+      if constexpr (C::QF) body_rm_qf<N, C>(w, s_mid, jz, j, sd, ok);
+      else if constexpr (C::FA) body_rm<N, C>(w, s_mid, jz, j, sd, ok);
+      else body_rm_exact<N, C>(w, s_mid, jz, j, sd, ok);
       continue;
     }
     StaticSteps<N, C, 1, U>::run(w, s_mid, jz);

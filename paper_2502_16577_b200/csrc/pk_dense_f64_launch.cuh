@@ -43,10 +43,10 @@ int launch_dense_f64(const DenseLaunch& a) {
   p.k = a.k;
   switch (a.policy) {
     case POL_DD:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB>>(a, p)
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB, 128, false, false, true>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_KAHAN:
-      if (a.exact) return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
       // a.variant (PK_DENSE_VARIANT, A/B runs): 0 step-major body (default),
       // 1 row-major body -- same bits, within 1 % (profiles/r02_k1_variants.txt;
       // 384-thread row-major blocks and 32-step bodies were no better)
@@ -54,10 +54,10 @@ int launch_dense_f64(const DenseLaunch& a) {
         return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
       return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_DQ:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB>>(a, p)
+      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB, 128, false, false, true>>(a, p)
                      : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_QQ:
-      if (a.exact) return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
       // row-major fast QQ (same bits) above n = 36, where the step-major body
       // spills: +12 % at n = 40, -3..5 % at n = 32..36
       // (profiles/r02_qq_variants.txt); PK_DENSE_VARIANT=1 forces it
