@@ -367,6 +367,9 @@ __device__ __forceinline__ void pair_body_rm(C128PairFast<N, C>& w, double s_mid
     w.xr[i] = vr;
     w.xi[i] = vi;
   }
+  // combine the halves term by term (independent), then sum the body's U
+  // terms as a pairwise tree: dependency depth 2 + log2(U) instead of 2U
+  double tr[U], ti[U];
 #pragma unroll
   for (int q = 1; q <= U; ++q) {
     double ar = __shfl_xor_sync(0xffffffffu, pr[q - 1], 1);
@@ -375,13 +378,19 @@ __device__ __forceinline__ void pair_body_rm(C128PairFast<N, C>& w, double s_mid
       ar = -ar;
       ai = -ai;
     }
-    const double r0 = q == 1 ? 0.0 : w.br, i0 = q == 1 ? 0.0 : w.bi;
-    const double nr = __fma_rn(ar, pr[q - 1], __fma_rn(-ai, pi[q - 1], r0));
-    const double ni = __fma_rn(ar, pi[q - 1], __fma_rn(ai, pr[q - 1], i0));
     const bool valid = q < U || okd;
-    w.br = valid ? nr : w.br;
-    w.bi = valid ? ni : w.bi;
+    tr[q - 1] = valid ? __fma_rn(ar, pr[q - 1], -__dmul_rn(ai, pi[q - 1])) : 0.0;
+    ti[q - 1] = valid ? __fma_rn(ar, pi[q - 1], __dmul_rn(ai, pr[q - 1])) : 0.0;
   }
+#pragma unroll
+  for (int w2 = 1; w2 < U; w2 <<= 1)
+#pragma unroll
+    for (int q = 0; q + w2 < U; q += 2 * w2) {
+      tr[q] = __dadd_rn(tr[q], tr[q + w2]);
+      ti[q] = __dadd_rn(ti[q], ti[q + w2]);
+    }
+  w.br = tr[0];
+  w.bi = ti[0];
 }
 
 template <int N, class C>
