@@ -474,6 +474,7 @@ void quantize_walk(const double* cols, const double* x0, int n, int comps, doubl
         int e = 0;
         std::frexp(bound, &e);  // bound < 2^e
         F = 52 - e;
+        if (F > 1074) F = 1074;  // subnormal rows: 2^-1074 is the finest grid there is
       }
       auto q = [&](double v) { return grid ? std::ldexp(std::nearbyint(std::ldexp(v, F)), -F) : v; };
       qx0[(size_t)comps * i + c] = q(x0[(size_t)comps * i + c]);

@@ -84,3 +84,19 @@ def test_zero_rows_and_bad_arguments():
                                 _native.dptr(x0)) == _native.PK_ERR_ARG
     assert lib.pk_quantize_walk(_native.dptr(cols), _native.dptr(x0), 64, 1, _native.dptr(cols),
                                 _native.dptr(x0)) == _native.PK_ERR_IMPOSSIBLE
+
+
+def test_subnormal_rows_stay_on_a_representable_grid():
+    n = 6
+    rng = np.random.default_rng(3)
+    cols = rng.uniform(0, 1, size=(n - 1) * n) * 1e-310  # subnormal entries
+    x0 = rng.uniform(-1, 1, size=n) * 1e-310
+    qc, qx = quantize(cols, x0, n, 1)
+    # the walk's states of grid values are exact sums
+    c2 = qc.reshape(n - 1, n)
+    for i in range(n):
+        x = qx[i]
+        exact = Fraction(qx[i])
+        for j in range(n - 1):
+            x, exact = x + c2[j, i], exact + Fraction(c2[j, i])
+            assert Fraction(x) == exact
