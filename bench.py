@@ -566,7 +566,10 @@ def run_b200(args, dist: Dist):
         roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": achieved_tf / peak_tf, "traffic": traffic,
                     "traffic_source": (f"DRAM bytes per launch of the same kernel from ncu --set "
-                                       f"full ({tsrc}); the walk reads only its <32 KB inputs"
+                                       f"full ({tsrc}, a 2^36-iterate launch): the walk reads its "
+                                       f"<32 KB inputs once; the rest is the deterministic tail "
+                                       f"tree's group partials (16 B per group of 32 chunks, "
+                                       f"written once and read back once)"
                                        if tsrc else None),
                     "note": f"algorithmic {wl.flops} flop/update x updates per launch / CUDA-event "
                             "time of that launch; peak = live DFMA microbenchmark (pk_fp64_peak); "
