@@ -62,7 +62,7 @@ extern "C" {
 #define PK_FLAG_SPARSE 2u /* real and integer walks: generate, compile (NVRTC) and cache a
                              per-matrix SpaRyser kernel that updates only the
                              flipped column's nonzeros (_loops.py:263-284) */
-#define PK_FLAG_PRECISE 4u /* dense real walks (pk_dense_f64, pk_dense_f64_chunks):
+#define PK_FLAG_PRECISE 4u /* dense real and complex walks (pk_dense_f64[_chunks], pk_dense_c128[_chunks]):
                               exact fixed-point row sums, double-double products
                               and sums -- reference-grade values (policy ignored,
                               ~12x the fast walk); the accuracy anchor at orders

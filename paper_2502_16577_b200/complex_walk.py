@@ -42,12 +42,15 @@ class DenseC128Problem:
 
     def walk(self, start: int, end: int, *, exact: bool = False,
              devices: Optional[Sequence[int]] = None, log2_chunk: int = 0,
-             stats: Optional[nat.RunStats] = None) -> Tuple[DoubleDouble, DoubleDouble]:
+             stats: Optional[nat.RunStats] = None,
+             precise: bool = False) -> Tuple[DoubleDouble, DoubleDouble]:
+        """precise=True (dense): exact fixed-point states per component,
+        double-double complex products and sums (PK_FLAG_PRECISE)."""
         lib = nat.load()
         out = np.zeros(4)
         dptr, nd, _keep = nat.devices_arg(devices)
         st = stats if stats is not None else nat.RunStats()
-        flags = nat.PK_FLAG_EXACT if exact else 0
+        flags = (nat.PK_FLAG_EXACT if exact else 0) | (nat.PK_FLAG_PRECISE if precise else 0)
         if self.sparse:
             rc = lib.pk_sparse_c128(nat.i64ptr(self.cptrs), nat.i64ptr(self.rids),
                                     nat.dptr(self.vals), self.n, nat.dptr(self.x0), start, end,
@@ -104,13 +107,31 @@ class DenseC128Problem:
         return p
 
 
-def complex_walk_total(m, devices=None, stats=None) -> complex:
+def _exact_p0(x0c) -> Tuple[DoubleDouble, DoubleDouble]:
+    """The g = 0 product of the (double) seed, exact in rationals, rounded to
+    double-double per component (the precise mode's p0)."""
+    from fractions import Fraction
+    pr, pi = Fraction(1), Fraction(0)
+    for v in x0c:
+        a, b = Fraction(float(v.real)), Fraction(float(v.imag))
+        pr, pi = pr * a - pi * b, pr * b + pi * a
+
+    def dd(f):
+        hi = float(f)
+        return DoubleDouble(hi, float(f - Fraction(hi)))
+    return dd(pr), dd(pi)
+
+
+def complex_walk_total(m, devices=None, stats=None, precise: bool = False) -> complex:
     prob = DenseC128Problem(m)
     n = prob.n
-    p0 = prob.p0()
-    re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+    if precise:
+        re, im = _exact_p0(prob.x0c)
+    else:
+        p0 = prob.p0()
+        re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
     if n > 1:
-        wr, wi = prob.walk(1, total_iterates(n), devices=devices, stats=stats)
+        wr, wi = prob.walk(1, total_iterates(n), devices=devices, stats=stats, precise=precise)
         re, im = dd_add(re, wr), dd_add(im, wi)
     sign = _sign_factor(n)
     return complex(re.hi * sign, im.hi * sign)

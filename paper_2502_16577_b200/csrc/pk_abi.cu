@@ -657,7 +657,7 @@ pk::SpaC128Spec spa_c128_spec(const double* cols, int n, bool exact) {
 }
 
 Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
-                     bool sparse = false) {
+                     bool sparse = false, bool precise = false) {
   Kind kd;
   kd.n = n;
   kd.streams = 2;
@@ -668,7 +668,7 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   const size_t nc = 2 * ncols_of(n);
   // fast modes walk the input rounded onto per-row, per-component grids
   std::shared_ptr<std::vector<double>> qbuf;
-  if (!exact && kd.logu > 0) {
+  if (!exact && !precise && kd.logu > 0) {
     qbuf = std::make_shared<std::vector<double>>(nc + 2 * n);
     quantize_walk(cols, x0, n, 2, qbuf->data(), qbuf->data() + nc);
     cols = qbuf->data();
@@ -678,7 +678,42 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   if (n > 1) std::memcpy(kd.input.data(), cols, (size_t)(n - 1) * n * 16);
   std::memcpy(kd.input.data() + nc, x0, (size_t)n * 16);
   const double* h_x0 = x0;
-  if (sparse && kd.logu > 0 && !pair) {
+  if (precise && n >= pk::kC128NMin) {
+    // precise mode: exact fixed-point states per component, double-double
+    // complex products and sums (pk_precise.cuh); images of the (unrounded)
+    // re and im parts back to back
+    if (kd.logu <= 0) kd.logu = 1;
+    const size_t fo = kd.input.size();
+    const size_t fw = fix_words_of(n);
+    kd.input.resize(fo + 2 * fw, 0.0);
+    std::vector<double> cr(ncols_of(n)), ci(ncols_of(n)), xr(n), xi(n);
+    for (size_t t = 0; t < (size_t)(n - 1) * n; ++t) {
+      cr[t] = cols[2 * t];
+      ci[t] = cols[2 * t + 1];
+    }
+    for (int i = 0; i < n; ++i) {
+      xr[i] = x0[2 * i];
+      xi[i] = x0[2 * i + 1];
+    }
+    fixed_image(cr.data(), xr.data(), n, reinterpret_cast<long long*>(kd.input.data() + fo));
+    fixed_image(ci.data(), xi.data(), n, reinterpret_cast<long long*>(kd.input.data() + fo + fw));
+    kd.fast = [=](DevCtx& c, const double* d_in, uint64_t chunk_lo, uint64_t groups,
+                  uint64_t g_end, int k, dd_t* gparts, dd_t* cparts, dd_t* out) {
+      pk::PreciseLaunch a{};
+      a.fix = reinterpret_cast<const long long*>(d_in + fo);
+      a.k = k;
+      a.chunk_lo = chunk_lo;
+      a.num_groups = groups;
+      a.g_end = g_end;
+      a.group_part = gparts;
+      a.chunk_part = cparts;
+      a.out = out;
+      a.counter = c.counter;
+      a.stream = c.stream;
+      a.sms = c.sms;
+      return pk::launch_dense_c128_precise(n, a);
+    };
+  } else if (sparse && kd.logu > 0 && !pair) {
     // SpaRyser: generated kernel over the nonzero pattern; packed nonzeros
     // (interleaved re, im) appended to the inputs
     auto sp = std::make_shared<pk::SpaC128Spec>(spa_c128_spec(cols, n, exact));
@@ -1249,7 +1284,7 @@ int pk_dense_c128(const double* cols, const double* x0, int n, uint64_t start, u
     if (!x0 || !out || (n > 1 && !cols)) fail(PK_ERR_ARG, "null pointer argument");
     check_range(n, start, end);
     Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0,
-                              (flags & PK_FLAG_SPARSE) != 0);
+                              (flags & PK_FLAG_SPARSE) != 0, (flags & PK_FLAG_PRECISE) != 0);
     dd_t res[2];
     drive(kd, start, end, log2_chunk, device_list(devices, ndev), res, stats);
     out[0] = res[0].hi;
@@ -1278,7 +1313,7 @@ int pk_dense_c128_chunks(const double* cols, const double* x0, int n, int log2_c
     check_n(n);
     if (!x0 || !cols || !out_total) fail(PK_ERR_ARG, "null pointer argument");
     Kind kd = dense_c128_kind(cols, x0, n, (flags & PK_FLAG_EXACT) != 0,
-                              (flags & PK_FLAG_SPARSE) != 0);
+                              (flags & PK_FLAG_SPARSE) != 0, (flags & PK_FLAG_PRECISE) != 0);
     dd_t tot[2];
     drive_chunks(kd, log2_chunk, chunk_lo, nchunks, device, reinterpret_cast<dd_t*>(out_chunks), tot);
     out_total[0] = tot[0].hi;

@@ -99,6 +99,8 @@ struct PreciseLaunch {
 };
 
 int launch_dense_f64_precise(int n, const PreciseLaunch& a);
+// complex: fix = the re image then the im image (two fixed_image layouts)
+int launch_dense_c128_precise(int n, const PreciseLaunch& a);
 
 // batched whole walks of `batch` matrices of order N (device inputs)
 struct DenseBatchLaunch {

@@ -261,12 +261,13 @@ def _real_walk_total(a: DenseMatrix, policy: AccumulatorPolicy, devices=None,
 def perm_nw(a: DenseMatrix, policy: "AccumulatorPolicy | str" = AccumulatorPolicy.DD,
             *, devices: Optional[Sequence[int]] = None, precise: bool = False) -> Scalar:
     """Permanent by the Gray walk over the 2^(n-1) half-space subsets,
-    computed on the GPU (kernels.py:297-324). precise=True (dense real,
-    n >= 11): exact fixed-point row sums with double-double products and sums
-    -- reference-grade, about 12x slower."""
+    computed on the GPU (kernels.py:297-324). precise=True (dense real or
+    complex, n >= 11): exact fixed-point row sums with double-double products
+    and sums -- reference-grade, about 10x (real) / 15x (complex) slower
+    (DESIGN.md §3)."""
     policy = as_policy(policy)
-    if precise and a.kind != KIND_REAL:
-        raise PolicyError("precise mode serves dense real matrices")
+    if precise and a.kind == KIND_INT:
+        raise PolicyError("precise mode serves real and complex matrices (integers are exact)")
     if a.kind == KIND_INT:
         from .integer import int_walk_total
         return int_walk_total(a, devices=devices)
@@ -274,7 +275,7 @@ def perm_nw(a: DenseMatrix, policy: "AccumulatorPolicy | str" = AccumulatorPolic
         if policy is not AccumulatorPolicy.DD:
             raise PolicyError("complex matrices support the plain-double policy only")
         from .complex_walk import complex_walk_total
-        return complex_walk_total(a, devices=devices)
+        return complex_walk_total(a, devices=devices, precise=precise)
     return _real_walk_total(a, policy, devices, precise=precise)
 
 

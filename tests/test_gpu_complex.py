@@ -105,3 +105,21 @@ def test_complex_sparse_equals_dense():
     m = pk.haar_unitary_block(14, 3)
     s = pk.dense_to_sparse(m)
     assert crel(pk.perm_spa(s), pk.perm_nw(m)) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [14, 20, 24])
+def test_complex_precise_mode_uniform_closed_form(n):
+    from fractions import Fraction
+    import math
+    a = complex(0.6, 0.7)
+    m = pk.DenseMatrix.from_rows([[a] * n for _ in range(n)])
+    got = pk.perm_nw(m, precise=True)
+    # n! a^n exactly (a's binary value), compared in rationals
+    ar, ai = Fraction(a.real), Fraction(a.imag)
+    pr, pi = Fraction(1), Fraction(0)
+    for _ in range(n):
+        pr, pi = pr * ar - pi * ai, pr * ai + pi * ar
+    f = math.factorial(n)
+    er, ei = f * pr, f * pi
+    err = math.hypot(float(Fraction(got.real) - er), float(Fraction(got.imag) - ei))
+    assert err <= 1e-13 * math.hypot(float(er), float(ei)), (n, got, err)

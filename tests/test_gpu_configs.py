@@ -278,3 +278,16 @@ def test_config4_haar32_fast_vs_exact_short_chunks():
     im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
     exact = complex(re.hi, im.hi) * pk.kernels._sign_factor(32)
     assert abs(fast - exact) <= REL_TOL * abs(exact), (fast, exact, abs(fast - exact) / abs(exact))
+
+
+def test_config4_haar32_fast_within_tolerance_and_closer_than_the_reference():
+    # complex precise mode (exact fixed-point states per component,
+    # double-double complex products and sums) as the truth
+    d = load("haar32_dd")
+    m = matrix(d["matrix"])
+    ref = _dec(d["value"], "complex128")
+    truth = pk.perm_nw(m, precise=True)
+    fast = pk.perm_nw(m)
+    assert abs(ref - truth) <= 1e-7 * abs(truth), (ref, truth)
+    assert abs(fast - truth) <= REL_TOL * abs(truth), (fast, truth, abs(fast - truth) / abs(truth))
+    assert abs(fast - truth) <= abs(ref - truth), (fast, ref, truth)
