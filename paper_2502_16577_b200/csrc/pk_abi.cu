@@ -662,7 +662,8 @@ Kind dense_c128_kind(const double* cols, const double* x0, int n, bool exact,
   kd.n = n;
   kd.streams = 2;
   const bool pair = c128_use_pair(n);
-  kd.logu = pair ? pk::c128_pair_logu(n)
+  kd.logu = pair ? ((exact || c128_variant() == 2) ? pk::c128_pair_logu(n)
+                                                   : pk::c128_pair_fast_logu(n))
                  : (n >= pk::kC128NMin && n <= pk::kC128NMax) ? c128_kernel_logu(n, exact) : 0;
   kd.chunks_log2 = 19;
   const size_t nc = 2 * ncols_of(n);
@@ -1617,7 +1618,8 @@ int pk_dense_c128_batch(const double* cols, const double* x0, int n, int batch, 
     int k = 0;
     if (n >= pk::kC128NMin) {
       const bool pair = c128_use_pair(n);  // K3p above K3's register limit
-      k = pk::batch_log2_chunk(n, pair ? pk::c128_pair_logu(n)
+      k = pk::batch_log2_chunk(n, pair ? ((flags & PK_FLAG_EXACT) ? pk::c128_pair_logu(n)
+                                                                 : pk::c128_pair_fast_logu(n))
                                   : (flags & PK_FLAG_EXACT) ? pk::c128_logu(n)
                                                             : pk::c128_fast_logu(n));
       const size_t groups = (size_t)((1ull << (n - 1 - k)) / 32);

@@ -44,7 +44,8 @@ int launch_c128_pair(const C128Launch& a) {
   // PK_C128_VARIANT=2 selects the step-major body, as for K3
   return a.variant == 2
              ? launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK>>(a)
-             : launch_c128_pair_cfg<N, C128Cfg<LOGU, false, MB, false, BLK, false, true>>(a);
+             : launch_c128_pair_cfg<N, C128Cfg<c128_pair_fast_logu(N), false, MB, false, BLK,
+                                               false, true>>(a);
 }
 
 template <int N, class C>
@@ -72,7 +73,8 @@ int launch_c128_pair_batch(const C128BatchLaunch& a) {
   constexpr int LOGU = c128_pair_logu(N);
   constexpr int BLK = c128_pair_block(N), MB = c128_pair_minb(N);
   if (a.exact) return launch_c128_pair_batch_cfg<N, C128Cfg<LOGU, true, MB, false, BLK>>(a);
-  return launch_c128_pair_batch_cfg<N, C128Cfg<LOGU, false, MB, false, BLK, false, true>>(a);
+  return launch_c128_pair_batch_cfg<N, C128Cfg<c128_pair_fast_logu(N), false, MB, false, BLK,
+                                                false, true>>(a);
 }
 
 }  // namespace pk

@@ -159,6 +159,9 @@ int launch_dense_c128(const C128Launch& a);
 // lane-pair complex kernel (pk_c128_pair.cuh): every order up to kDenseNMax;
 // 4*ceil(N/2) registers of state per lane
 constexpr int c128_pair_logu(int N) { return N <= 48 ? 2 : 1; }
+// the fast (row-major) pair bodies are twice as long (A/B in
+// profiles/r02_c128_pair_logu.txt)
+constexpr int c128_pair_fast_logu(int N) { return N <= 42 ? 4 : 3; }
 constexpr int c128_pair_block(int N) { return 256; }
 constexpr int c128_pair_minb(int N) { return N <= 32 ? 2 : 1; }
 

@@ -37,9 +37,14 @@ C128_PAIR_N_MAX = 63
 
 
 def c128_pair_logu(n: int) -> int:
+    """K3p exact-mode body length (log2)."""
     return 2 if n <= 48 else 1
+
+
+def c128_pair_fast_logu(n: int) -> int:
+    return 4 if n <= 42 else 3
 
 
 def c128_register_logu(n: int) -> int:
     """Body length exponent of the fast complex register kernel at order n."""
-    return c128_fast_logu(n) if n <= C128_N_MAX else c128_pair_logu(n)
+    return c128_fast_logu(n) if n <= C128_N_MAX else c128_pair_fast_logu(n)

@@ -77,7 +77,7 @@ import json, sys
 sys.path.insert(0, %r)
 import paper_2502_16577_b200 as pk
 from paper_2502_16577_b200.complex_walk import DenseC128Problem
-from paper_2502_16577_b200.csrc_params import c128_pair_logu
+from paper_2502_16577_b200.csrc_params import c128_pair_fast_logu, c128_pair_logu
 from paper_2502_16577_b200.kernels import _sign_factor
 from paper_2502_16577_b200.precision import DoubleDouble, dd_add
 n = int(sys.argv[1])
@@ -85,7 +85,7 @@ out = []
 for exact in (False, True):
     ms = [pk.haar_unitary_block(n, 60 + s, m=2 * n) for s in range(3)]
     got = pk.permanent_batch(ms, exact=exact)
-    k = max(n - 1 - 10, c128_pair_logu(n) + 1)
+    k = max(n - 1 - 10, (c128_pair_logu(n) if exact else c128_pair_fast_logu(n)) + 1)
     for m, g in zip(ms, got):
         prob = DenseC128Problem(m)
         wr, wi = prob.walk(1, (1 << (n - 1)) - 1, exact=exact, log2_chunk=k)
