@@ -131,9 +131,10 @@ constexpr int kC128NMax = 40;
 // complex state is 4N registers; longer bodies make ptxas interleave more
 // product chains than the register file holds, so bodies stay short
 constexpr int c128_logu(int N) { return N <= 32 ? 2 : 1; }
-// fast mode walks row-major bodies of twice that length (C128Cfg::RM):
-// +3..6 % at n = 28..36 (profiles/r02_c128_variants_rm.txt)
-constexpr int c128_fast_logu(int N) { return c128_logu(N) + 1; }
+// fast mode walks row-major 8-step bodies (C128Cfg::RM) at every order:
+// +3..8 % over the step-major bodies at n = 28..40
+// (profiles/r02_c128_variants_rm.txt, r02_c128_fast_logu.txt)
+constexpr int c128_fast_logu(int N) { return 3; }
 constexpr int c128_minb(int N) { return N <= 32 ? 2 : 1; }
 
 struct C128Launch {

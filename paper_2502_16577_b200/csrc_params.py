@@ -19,8 +19,8 @@ def c128_logu(n: int) -> int:
 
 
 def c128_fast_logu(n: int) -> int:
-    """K3's fast (row-major) body length: twice the exact mode's."""
-    return c128_logu(n) + 1
+    """K3's fast (row-major) body length: 8 steps at every order."""
+    return 3
 
 
 def auto_log2_chunk(bit_len: int, logu: int, chunks_log2: int) -> int:

@@ -179,8 +179,8 @@ def test_csrc_params_mirror():
     assert cp.c128_logu(32) == 2 and cp.c128_logu(33) == 1
     assert "constexpr int kC128NMax = 40;" in text and cp.C128_N_MAX == 40
     assert "constexpr int c128_pair_logu(int N) { return N <= 48 ? 2 : 1; }" in text
-    assert "constexpr int c128_fast_logu(int N) { return c128_logu(N) + 1; }" in text
-    assert cp.c128_register_logu(40) == 2 and cp.c128_register_logu(41) == 4
+    assert "constexpr int c128_fast_logu(int N) { return 3; }" in text
+    assert cp.c128_register_logu(40) == 3 and cp.c128_register_logu(41) == 4
     assert "constexpr int c128_pair_fast_logu(int N) { return N <= 42 ? 4 : 3; }" in text
     assert cp.c128_pair_fast_logu(42) == 4 and cp.c128_pair_fast_logu(43) == 3
     assert cp.dense_logu(50) == 4 and cp.dense_logu(51) == 3
