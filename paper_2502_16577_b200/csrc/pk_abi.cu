@@ -398,12 +398,13 @@ int dispatch_c128_pair_batch(int n, const pk::C128BatchLaunch& a) {
 // Complex register kernel for order n: K3 (one thread per chunk) up to
 // kC128NMax, the lane-pair kernel K3p above (PK_C128_PAIR=1 selects K3p for
 // every order, for A/B runs).
-// K1's fast body schedule (PK_DENSE_VARIANT, A/B runs): 0 step-major
-// (default), 1 row-major (pk_dense_f64_launch.cuh)
+// K1's fast body schedule (PK_DENSE_VARIANT, A/B runs): 0 the default
+// (row-major above n = 36), 1 row-major, 2 step-major (pk_dense_f64_launch.cuh)
 int dense_variant() {
   static const int v = [] {
     const char* e = getenv("PK_DENSE_VARIANT");
-    return (e && atoi(e) == 1) ? 1 : 0;
+    const int r = e ? atoi(e) : 0;
+    return (r == 1 || r == 2) ? r : 0;
   }();
   return v;
 }

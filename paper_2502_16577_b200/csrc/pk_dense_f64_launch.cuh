@@ -47,10 +47,10 @@ int launch_dense_f64(const DenseLaunch& a) {
                      : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_KAHAN:
       if (a.exact) return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
-      // a.variant (PK_DENSE_VARIANT, A/B runs): 0 step-major body (default),
-      // 1 row-major body -- same bits, within 1 % (profiles/r02_k1_variants.txt;
-      // 384-thread row-major blocks and 32-step bodies were no better)
-      if (a.variant == 1)
+      // row-major body above n = 36 (same bits; +0.2 % at n = 40, +1 % at
+      // n = 48), step-major below (-0.3 % at n = 36) -- profiles/r02_k1_variants.txt;
+      // PK_DENSE_VARIANT=1 forces row-major, 2 step-major (A/B runs)
+      if ((N > 36 && a.variant != 2) || a.variant == 1)
         return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
       return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_DQ:
