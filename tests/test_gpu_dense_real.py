@@ -213,3 +213,17 @@ def test_precise_mode_uniform_closed_form(n):
     exact = math.factorial(n) * Fraction(0.91) ** n
     got = pk.perm_nw(pk.uniform(n, 0.91), precise=True)
     assert float(abs(Fraction(got) - exact) / exact) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [36, 40])
+def test_uniform_closed_form_large(n):
+    # uniform(n, 0.91): every x_i is equal, so the double product x^n rounds
+    # the same way for every subset of one size and product rounding does not
+    # average out under KAHAN / DQ / DD (2.3e-10 at n = 40); QQ's double-double
+    # product removes it (2.8e-13; the paper: 6.5e-11 at n = 40)
+    exact = math.factorial(n) * Fraction(0.91) ** n
+    m = pk.uniform(n, 0.91)
+    err_qq = float(abs(Fraction(pk.perm_nw(m, "qq")) - exact) / exact)
+    assert err_qq <= 1e-12, err_qq
+    err_k = float(abs(Fraction(pk.perm_nw(m, "kahan")) - exact) / exact)
+    assert err_k <= 5e-10, err_k
