@@ -505,8 +505,10 @@ void fixed_image(const double* cols, const double* x0, int n, long long* out) {
       int e = 0;
       std::frexp(bound * (1.0 + 0x1p-40), &e);  // bound (with slack) < 2^e
       F = 62 - e;
-      if (F > 1000) F = 1000;    // 2^-F stays a normal double
-      if (F < -1000) F = -1000;
+      // 2^-F must be a double: at most 2^-1074, where subnormal entries are
+      // integers on the grid (bound < 2^-1022 keeps X below 2^52); F >= -962
+      // holds for every finite bound
+      if (F > 1074) F = 1074;
     }
     for (int j = 0; j < n - 1; ++j)
       A[(size_t)j * n + i] = std::llrint(std::ldexp(cols[(size_t)j * n + i], F));
