@@ -1,4 +1,6 @@
-"""Accuracy of the fast dense real walk vs the state rebuild period
+"""[historical (round 1 / early round 2): the x rebuild and PK_REBUILD_LOG2 were removed when the fast walks moved to exact grid-rounded states; kept to document profiles/r02_accuracy_*_rb*.txt]
+
+Accuracy of the fast dense real walk vs the state rebuild period
 (PK_REBUILD_LOG2): relative error of uniform(n, 0.91) against the closed form
 n! a^n, and the random [0,1) value, per policy. One process per setting
 (the period is read once per process).
