@@ -128,3 +128,23 @@ def test_spa_structure_errors():
         prob.rids = bad
         with pytest.raises(pk.StructureError):
             prob.walk(1, K.total_iterates(n), AccumulatorPolicy.DD)
+
+
+@pytest.mark.parametrize("policy", ["kahan", "qq"])
+def test_sparse_exact_equals_dense_exact_on_non_power_of_two_groups(policy):
+    # the tail tree has a fixed leaf count (pk_reduce.cuh
+    # kTreeLeaves), so the generated sparse kernel (one 384/256-thread block
+    # per SM from n = 33) and the dense kernel (128-thread blocks in exact
+    # mode) fold the same group partials identically even when the range's
+    # group count is not a power of two
+    from paper_2502_16577_b200.kernels import DenseF64Problem, SparseF64Problem
+    n = 36
+    s = pk.random_sparse_real(n, 0.35, 11, 0.0, 1.0)
+    sp, dn = SparseF64Problem(s), DenseF64Problem(pk.sparse_to_dense(s))
+    pol = AccumulatorPolicy.parse(policy)
+    k = 12
+    start = 1 + 5 * (1 << k) + 77          # unaligned head
+    end = start + 37 * 32 * (1 << k) + 123  # 37 groups of 32 chunks + tail
+    a = sp.walk(start, end, pol, exact=True, log2_chunk=k)
+    b = dn.walk(start, end, pol, exact=True, log2_chunk=k)
+    assert (a.hi, a.lo) == (b.hi, b.lo)
