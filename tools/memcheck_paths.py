@@ -41,4 +41,7 @@ for n in (32, 41, 63):
     print(n, hp.walk(1, 1 << 21), hp.chunks(7, 32, 32, exact=True)[1])
 print(IntProblem(pk.dense_to_sparse(pk.random_binary(40, 5, 0.3))).walk(1, 1 << 22)[0])
 print(DenseF64Problem(pk.random_real(40, 4, 0.0, 1.0)).chunks(8, 64, 32, pk.AccumulatorPolicy.QQ, exact=True)[1])
+hp36 = DenseC128Problem(pk.haar_unitary_block(36, 3, m=72))
+print(hp36.walk(1, 1 << 21), hp36.walk(1, 1 << 16, precise=True))
+print(DenseF64Problem(pk.random_real(48, 4, 0.0, 1.0)).walk(1, 1 << 22, pk.AccumulatorPolicy.QQ))
 print("memcheck paths done")
