@@ -41,7 +41,9 @@ def permanent(matrix, policy="dd", workers: int = 1, aligned: bool = True, *, de
     The reference splits the walk over ``workers`` CPU threads; here the walk
     is split into GPU-sized aligned chunks regardless, and ``workers`` > 1
     spreads it over that many GPUs (contiguous Gray-code ranges, fixed-order
-    host reduction). ``devices`` selects explicit CUDA ordinals.
+    host reduction). ``devices`` selects explicit CUDA ordinals. ``aligned``
+    is accepted for compatibility: the GPU split is always the aligned
+    (power-of-two) tiling, which permkit's ``aligned=True`` default also uses.
     """
     from . import _native
     from .precision import as_policy
