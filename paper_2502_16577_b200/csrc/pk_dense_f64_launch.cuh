@@ -43,8 +43,11 @@ int launch_dense_f64(const DenseLaunch& a) {
   p.k = a.k;
   switch (a.policy) {
     case POL_DD:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB, 128, false, false, true>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
+      // row-major above n = 36, as KAHAN (same bits)
+      if ((N > 36 && a.variant != 2) || a.variant == 1)
+        return launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
+      return launch_cfg<N, DenseCfg<POL_DD, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_KAHAN:
       if (a.exact) return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
       // row-major body above n = 36 (same bits; +0.2 % at n = 40, +1 % at
@@ -54,8 +57,10 @@ int launch_dense_f64(const DenseLaunch& a) {
         return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
       return launch_cfg<N, DenseCfg<POL_KAHAN, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_DQ:
-      return a.exact ? launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB, 128, false, false, true>>(a, p)
-                     : launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);
+      if (a.exact) return launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
+      if ((N > 36 && a.variant != 2) || a.variant == 1)
+        return launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true, false, true>>(a, p);
+      return launch_cfg<N, DenseCfg<POL_DQ, 1, LOGU, true, BMB, BLK, true>>(a, p);
     case POL_QQ:
       if (a.exact) return launch_cfg<N, DenseCfg<POL_QQ, 1, LOGU, false, MB, 128, false, false, true>>(a, p);
       // row-major fast QQ (same bits) above n = 36, where the step-major body

@@ -26,8 +26,10 @@ out = {}
 for n in (24, 34, 40):
     m = pk.DenseMatrix.from_array(np.random.default_rng(n).uniform(0.0, 1.0, size=(n, n)))
     T = (1 << (n - 1)) - 1
-    p = pk.kernels.DenseF64Problem(m).walk(1, min(T, (1 << 34) - 5), pk.AccumulatorPolicy.KAHAN)
-    out["real%%d" %% n] = [p.hi.hex(), p.lo.hex()]
+    for pol in ("dd", "kahan", "dq"):
+        p = pk.kernels.DenseF64Problem(m).walk(1, min(T, (1 << 34) - 5),
+                                               pk.AccumulatorPolicy.parse(pol))
+        out["real%%d_%%s" %% (n, pol)] = [p.hi.hex(), p.lo.hex()]
 for n in (20, 30, 44):
     h = pk.haar_unitary_block(n, 3, m=2 * n)
     T = (1 << (n - 1)) - 1
