@@ -385,17 +385,16 @@ class Workload:
                                                      dd_pairwise)
         n = self.n
         if self.kind in ("dense", "sparse"):
-            from paper_2502_16577_b200.kernels import SparseF64Problem
+            from paper_2502_16577_b200.kernels import SparseF64Problem, fast_p0
             prob = DenseF64Problem(self.m) if self.kind == "dense" else SparseF64Problem(self.m)
-            p0 = policy_product(prob.x0, AccumulatorPolicy.parse(self.policy))
-            acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+            acc = fast_p0(prob.cols, prob.x0, n, self.policy)  # the rounded seed the walk uses
             acc = dd_add(acc, dd_pairwise([tuple(g[:2]) for g in gathered]))
             return (acc.hi * _sign_factor(n)).hex()
         if self.kind == "haar":
-            from paper_2502_16577_b200.complex_walk import DenseC128Problem
-            p0 = DenseC128Problem(self.m).p0()
-            re = dd_add(DoubleDouble(p0.real, 0.0), dd_pairwise([tuple(g[0:2]) for g in gathered]))
-            im = dd_add(DoubleDouble(p0.imag, 0.0), dd_pairwise([tuple(g[2:4]) for g in gathered]))
+            from paper_2502_16577_b200.complex_walk import DenseC128Problem, fast_p0
+            p0r, p0i = fast_p0(DenseC128Problem(self.m))
+            re = dd_add(p0r, dd_pairwise([tuple(g[0:2]) for g in gathered]))
+            im = dd_add(p0i, dd_pairwise([tuple(g[2:4]) for g in gathered]))
             s = _sign_factor(n)
             return [(re.hi * s).hex(), (im.hi * s).hex()]
         from paper_2502_16577_b200.integer import IntProblem, _signed, finalize_int

@@ -61,9 +61,13 @@ def real_batch_arrays(A: np.ndarray, policy: AccumulatorPolicy, device: int = 0,
                                        nat.PK_FLAG_EXACT if exact else 0, device, nat.dptr(out), st)
     nat.check(rc, "pk_dense_f64_batch")
     res = []
+    from .kernels import fast_p0
     for i in range(b):
-        p0 = policy_product(x0[i], policy)
-        acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+        if exact:
+            p0 = policy_product(x0[i], policy)
+            acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+        else:  # the rounded seed the device walks, exact product (kernels.fast_p0)
+            acc = fast_p0(cols[i].reshape(-1) if n > 1 else np.zeros(1), x0[i], n, policy)
         if n > 1:
             acc = dd_add(acc, DoubleDouble(float(out[2 * i]), float(out[2 * i + 1])))
         res.append(acc.hi * _sign_factor(n))
@@ -86,11 +90,24 @@ def complex_batch_arrays(A: np.ndarray, device: int = 0, exact: bool = False,
     nat.check(rc, "pk_dense_c128_batch")
     res = []
     sign = _sign_factor(n)
+    from .complex_walk import _exact_p0
+    from .kernels import quantized_seed
     for i in range(b):
-        p = complex(1.0)
-        for v in x0[i]:
-            p = p * complex(v)
-        re, im = DoubleDouble(p.real, 0.0), DoubleDouble(p.imag, 0.0)
+        if exact:
+            p = complex(1.0)
+            for v in x0[i]:
+                p = p * complex(v)
+            re, im = DoubleDouble(p.real, 0.0), DoubleDouble(p.imag, 0.0)
+        elif n < 11:  # the reference loop's walk and product
+            p = complex(1.0)
+            for v in x0[i]:
+                p = p * complex(v)
+            re, im = DoubleDouble(p.real, 0.0), DoubleDouble(p.imag, 0.0)
+        else:  # the rounded seed the device walks (complex_walk.fast_p0)
+            xs = quantized_seed(np.ascontiguousarray(cols[i]).reshape(-1).view(np.float64),
+                                np.ascontiguousarray(x0[i]).view(np.float64), n,
+                                comps=2).view(np.complex128)
+            re, im = _exact_p0(xs)
         if n > 1:
             re = dd_add(re, DoubleDouble(float(out[4 * i]), float(out[4 * i + 1])))
             im = dd_add(im, DoubleDouble(float(out[4 * i + 2]), float(out[4 * i + 3])))

@@ -122,14 +122,23 @@ def _exact_p0(x0c) -> Tuple[DoubleDouble, DoubleDouble]:
     return dd(pr), dd(pi)
 
 
+def fast_p0(prob: "DenseC128Problem") -> Tuple[DoubleDouble, DoubleDouble]:
+    """g = 0 term of a fast complex walk: the exact product of the seed the
+    device walks (grid-rounded per component from n = 11), per component in
+    double-double (as kernels.fast_p0)."""
+    from .kernels import quantized_seed
+    n = prob.n
+    if n < 11:  # below the register kernels the walk is the reference's loop
+        p0 = prob.p0()
+        return DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+    q = quantized_seed(prob.cols, prob.x0, n, comps=2)
+    return _exact_p0(q.view(np.complex128))
+
+
 def complex_walk_total(m, devices=None, stats=None, precise: bool = False) -> complex:
     prob = DenseC128Problem(m)
     n = prob.n
-    if precise:
-        re, im = _exact_p0(prob.x0c)
-    else:
-        p0 = prob.p0()
-        re, im = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+    re, im = _exact_p0(prob.x0c) if precise else fast_p0(prob)
     if n > 1:
         wr, wi = prob.walk(1, total_iterates(n), devices=devices, stats=stats, precise=precise)
         re, im = dd_add(re, wr), dd_add(im, wi)

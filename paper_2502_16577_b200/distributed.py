@@ -15,7 +15,7 @@ from __future__ import annotations
 
 from typing import Callable, List, Optional, Sequence, Tuple
 
-from .kernels import DenseF64Problem, _sign_factor, policy_product, total_iterates
+from .kernels import DenseF64Problem, _sign_factor, fast_p0, policy_product, total_iterates
 from .matrix import DenseMatrix, coerce_matrix
 from .precision import AccumulatorPolicy, DoubleDouble, as_policy, dd_add, dd_pairwise
 
@@ -35,8 +35,8 @@ def combine_real(m: DenseMatrix, policy: AccumulatorPolicy,
                  partials: Sequence[Tuple[float, float]]) -> float:
     """g = 0 term + pairwise tree over the rank partials (rank order), times
     the global sign -- the same tree the single-device reduction builds."""
-    p0 = policy_product(DenseF64Problem(m).x0, policy)
-    acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+    prob = DenseF64Problem(m)
+    acc = fast_p0(prob.cols, prob.x0, m.n, policy)  # the rounded seed the fast walks use
     if partials:
         acc = dd_add(acc, dd_pairwise([tuple(p) for p in partials]))
     return acc.hi * _sign_factor(m.n)

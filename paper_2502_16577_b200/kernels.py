@@ -130,6 +130,44 @@ def policy_product(xs, policy: AccumulatorPolicy) -> Union[float, DoubleDouble]:
     return p
 
 
+def quantized_seed(cols: np.ndarray, x0: np.ndarray, n: int, comps: int = 1) -> np.ndarray:
+    """The seed x0 as the fast kernels walk it: rounded onto the same per-row
+    (per component) grids as the columns (pk_quantize_walk; DESIGN.md §3
+    "Exact states"). Host-only."""
+    c = np.ascontiguousarray(cols, dtype=np.float64).reshape(-1)
+    x = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1)
+    qc = np.zeros_like(c)
+    qx = np.zeros_like(x)
+    nat.check(nat.load().pk_quantize_walk(nat.dptr(c), nat.dptr(x), n, comps, nat.dptr(qc),
+                                          nat.dptr(qx)), "pk_quantize_walk")
+    return qx
+
+
+def _dd_of(f) -> DoubleDouble:
+    hi = float(f)
+    from fractions import Fraction
+    return DoubleDouble(hi, float(f - Fraction(hi)))
+
+
+def fast_p0(cols: np.ndarray, x0: np.ndarray, n: int,
+            policy: "AccumulatorPolicy | str" = AccumulatorPolicy.DD) -> DoubleDouble:
+    """The g = 0 term of a fast walk: the exact product of the seed the device
+    walks (grid-rounded from n = 11, where the register kernels start),
+    rounded once to double-double. It is the largest single term of the
+    cancelling sum, so it must belong to the same (rounded) matrix as the
+    walk and carry no product rounding: 3.4e-12 of the n = 40 error under QQ
+    and more under the double-product policies came from the seed being the
+    unrounded one (tools/quantization_effect.py)."""
+    from fractions import Fraction
+    if n < 11:  # below the register kernels the walk is the reference's loop
+        p0 = policy_product(x0, as_policy(policy))
+        return p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+    p = Fraction(1)
+    for v in quantized_seed(cols, x0, n):
+        p *= Fraction(float(v))
+    return _dd_of(p)
+
+
 def seed_accumulator(p0, policy: AccumulatorPolicy) -> Tuple[float, float]:
     if as_policy(policy) is AccumulatorPolicy.QQ:
         return p0.hi, p0.lo
@@ -249,9 +287,10 @@ def _real_walk_total(a: DenseMatrix, policy: AccumulatorPolicy, devices=None,
                      stats: Optional[nat.RunStats] = None, precise: bool = False) -> float:
     n = a.n
     prob = DenseF64Problem(a)
-    # precise mode: the g = 0 product in double-double as well
-    p0 = policy_product(prob.x0, AccumulatorPolicy.QQ if precise else policy)
-    acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+    # precise mode: the g = 0 product in double-double of the input's seed;
+    # fast mode: the exact product of the grid-rounded seed the device walks
+    acc = policy_product(prob.x0, AccumulatorPolicy.QQ) if precise else \
+        fast_p0(prob.cols, prob.x0, n, policy)
     if n > 1:
         acc = dd_add(acc, prob.walk(1, total_iterates(n), policy, devices=devices, stats=stats,
                                     precise=precise))
@@ -299,8 +338,7 @@ def perm_spa(s: SparsePair, policy: "AccumulatorPolicy | str" = AccumulatorPolic
 def _real_walk_total_sparse(s: SparsePair, policy, devices) -> float:
     n = s.n
     prob = SparseF64Problem(s)
-    p0 = policy_product(prob.x0, policy)
-    acc = p0 if isinstance(p0, DoubleDouble) else DoubleDouble(float(p0), 0.0)
+    acc = fast_p0(prob.cols, prob.x0, n, policy)
     if n > 1:
         acc = dd_add(acc, prob.walk(1, total_iterates(n), policy, devices=devices))
     return acc.hi * _sign_factor(n)

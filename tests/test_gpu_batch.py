@@ -8,7 +8,7 @@ import golden_io as gio
 import paper_2502_16577_b200 as pk
 from paper_2502_16577_b200 import _native
 from paper_2502_16577_b200.csrc_params import batch_log2_chunk, dense_logu
-from paper_2502_16577_b200.kernels import DenseF64Problem, policy_product, _sign_factor
+from paper_2502_16577_b200.kernels import DenseF64Problem, fast_p0, policy_product, _sign_factor
 from paper_2502_16577_b200.precision import AccumulatorPolicy, DoubleDouble, dd_add
 
 pytestmark = pytest.mark.gpu
@@ -24,8 +24,7 @@ def test_batch_equals_single_launch_bitwise(n, policy):
     for m, g in zip(ms, got):
         prob = DenseF64Problem(m)
         part = prob.walk(1, pk.total_iterates(n), pol, log2_chunk=k)
-        p0 = policy_product(prob.x0, pol)
-        acc = dd_add(p0 if isinstance(p0, DoubleDouble) else DoubleDouble(p0, 0.0), part)
+        acc = dd_add(fast_p0(prob.cols, prob.x0, n, pol), part)
         assert g == acc.hi * _sign_factor(n)
 
 
@@ -76,9 +75,14 @@ def test_complex_batch_equals_single_launch_bitwise(n, exact):
     for m, g in zip(ms, got):
         prob = DenseC128Problem(m)
         wr, wi = prob.walk(1, pk.total_iterates(n), exact=exact, log2_chunk=k)
-        p0 = prob.p0()
-        re = dd_add(DoubleDouble(p0.real, 0.0), wr)
-        im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+        if exact:
+            p0 = prob.p0()
+            r0, i0 = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+        else:
+            from paper_2502_16577_b200.complex_walk import fast_p0 as cfast_p0
+            r0, i0 = cfast_p0(prob)
+        re = dd_add(r0, wr)
+        im = dd_add(i0, wi)
         s = _sign_factor(n)
         assert g == complex(re.hi * s, im.hi * s), (n, g)
 

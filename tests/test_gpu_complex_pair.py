@@ -89,9 +89,14 @@ for exact in (False, True):
     for m, g in zip(ms, got):
         prob = DenseC128Problem(m)
         wr, wi = prob.walk(1, (1 << (n - 1)) - 1, exact=exact, log2_chunk=k)
-        p0 = prob.p0()
-        re = dd_add(DoubleDouble(p0.real, 0.0), wr)
-        im = dd_add(DoubleDouble(p0.imag, 0.0), wi)
+        if exact:
+            p0 = prob.p0()
+            r0, i0 = DoubleDouble(p0.real, 0.0), DoubleDouble(p0.imag, 0.0)
+        else:
+            from paper_2502_16577_b200.complex_walk import fast_p0
+            r0, i0 = fast_p0(prob)
+        re = dd_add(r0, wr)
+        im = dd_add(i0, wi)
         s = _sign_factor(n)
         out.append([g.real.hex(), g.imag.hex(), (re.hi * s).hex(), (im.hi * s).hex()])
 print(json.dumps(out))
